@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""bench.py — Soft-DTW DP cells/s (fwd+bwd) on B200, one JSON line on rank 0.
+
+Metric (BASELINE.json): DP cells/sec (fwd+bwd, fused & unfused) at B=32 vs
+L, D; peak HBM MB; 1/2/4/8 GPU.  cells/s = B*N*M / t(fwd+bwd), where one
+step = loss + grad_x + grad_y of the whole batch (sdtw_with_gradients,
+backward.hpp:276-304).
+
+Default workload = BASELINE.json configs[1]: B=32, N=M=1024, D=128,
+gamma=0.1, FUSED (the headline `value`), with the UNFUSED mode of the same
+config measured in the same run (`unfused`).  `--config c3` runs the
+north-star case (L=4096, gamma=0.01).
+
+Arms:
+  (default)         this engine (libsdtw_b200.so through the C-ABI).
+  --impl reference  the reference's own CPU implementation (oracle/_ref,
+                    compiled from the unmodified reference sources) with all
+                    host threads, rank 0 only.
+
+Multi-GPU: launched by torchrun, one rank per GPU; pairs are independent so
+every rank runs its own B=32 batch with no collective on the data path
+(weak scaling); time = max over ranks of the device-timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(B=32, L=256, D=128, gamma=1.0),
+    "c2": dict(B=32, L=1024, D=128, gamma=0.1),
+    "c3": dict(B=32, L=4096, D=128, gamma=0.01),
+    "c4": dict(B=32, L=256, D=1024, gamma=1.0),
+}
+METRIC = "DP cells/sec (fwd+bwd, fused & unfused) at B=32 vs L,D; peak HBM MB; 1/2/4/8 GPU"
+SM_COUNT = 148
+MUFU_PER_CLK_SM = 16
+# algorithmic MUFU work per DP cell
+MUFU_FWD, MUFU_BWD = 3, 4
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_rate(cfg, fused, threads, reps, warmup, max_pairs=None):
+    """The reference's run_bench_row (bench.hpp:52-107), fp32, `threads`
+    host threads.  Returns (cells/s, mean ms, sample description)."""
+    import oracle
+    ref = oracle.Reference()
+    B = cfg["B"] if max_pairs is None else min(cfg["B"], max_pairs)
+    rc, mean_ms, std_ms, peak, loss0 = ref.run_bench_row(B, cfg["L"], cfg["D"], cfg["gamma"],
+                                                          fused=fused, repeats=reps,
+                                                          warmup=warmup, threads=threads)
+    if rc != 0:
+        raise RuntimeError(f"reference run_bench_row failed rc={rc}")
+    cells = B * cfg["L"] * cfg["L"]
+    sample = (f"reference run_bench_row fp32 {'fused' if fused else 'unfused'} B={B} "
+              f"L={cfg['L']} D={cfg['D']} gamma={cfg['gamma']}, {reps} timed reps after "
+              f"{warmup} warm-up, threads={threads}")
+    return cells / (mean_ms / 1e3), mean_ms, sample
+
+
+def _ref_pairs_for(cfg):
+    # bound one reference step to ~10-20 s of host work (SURVEY.md §6.3:
+    # ~1.7e7 cells/s unfused, ~8e6 fused on 8 threads)
+    per_pair = cfg["L"] * cfg["L"]
+    return max(1, min(cfg["B"], int(8e7 // per_pair)))
+
+
+def run_reference_arm(args, cfg):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    fused = args.mode == "fused"
+    pairs = _ref_pairs_for(cfg)
+    times = []
+    val = None
+    sample = None
+    for it in range(args.warmup + args.steps):
+        v, ms, sample = cpu_reference_rate(cfg, fused, threads, 1, 0, max_pairs=pairs)
+        if it >= args.warmup:
+            times.append(ms)
+    ms = sum(times) / len(times)
+    cells = pairs * cfg["L"] * cfg["L"]
+    val = cells / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "cells/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) (reference bench generator, mt19937_64 seed 42)",
+        "config": _config_dict(args, cfg, ws),
+        "cpu_baseline": {"value": val, "unit": "cells/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(args, cfg, ws):
+    return {"workload": f"{args.config}: B={cfg['B']} N=M={cfg['L']} D={cfg['D']} "
+                        f"gamma={cfg['gamma']} {args.mode} fwd+bwd (loss, grad_x, grad_y)",
+            "B_per_gpu": cfg["B"], "global_batch": cfg["B"] * ws, "N": cfg["L"], "M": cfg["L"],
+            "D": cfg["D"], "gamma": cfg["gamma"], "cost_mode": args.mode,
+            "backward_space": "log", "parallelism": f"dp{ws} (pairs sharded, no collective)",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+def time_engine(eng, torch, x, y, outs, fused, gamma, steps, warmup, flush):
+    """Device-timed steps (CUDA events on the engine stream = torch's current
+    stream).  Returns (total_ms, per-phase ms sums, launches, peak bytes)."""
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        eng.sdtw_with_gradients(x, y, gamma, fused=fused, out=outs, sync=False)
+    torch.cuda.synchronize()
+    eng.reset_peak()
+    eng.enable_timing(True)
+    phases = {}
+    total = 0.0
+    eng.reset_launches()
+    launches = 0
+    for _ in range(steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        eng.sdtw_with_gradients(x, y, gamma, fused=fused, out=outs, sync=False)
+        e.record(stream)
+        e.synchronize()
+        total += s.elapsed_time(e)
+        for k, v in eng.phase_times().items():
+            phases[k] = phases.get(k, 0.0) + v
+        launches = eng.launches
+    eng.enable_timing(False)
+    return total, phases, launches, eng.mem_stats()[1]
+
+
+def run_engine_arm(args, cfg):
+    import numpy as np
+    import torch
+    from paper_2602_17206_b200 import Engine
+    from paper_2602_17206_b200.build import build
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    if rank == 0:
+        build()
+    if ws > 1:
+        dist.barrier()
+    eng = Engine(local)
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)
+    B, L, D, gamma = cfg["B"], cfg["L"], cfg["D"], cfg["gamma"]
+    gen = torch.Generator(device="cuda").manual_seed(42 + rank)
+    x = torch.randn((B, L, D), generator=gen, device="cuda", dtype=torch.float32)
+    y = torch.randn((B, L, D), generator=gen, device="cuda", dtype=torch.float32)
+    outs = (torch.empty(B, device="cuda"), torch.empty((B, L, D), device="cuda"),
+            torch.empty((B, L, D), device="cuda"))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    fused = args.mode == "fused"
+
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    total_ms, phases, launches, peak = time_engine(eng, torch, x, y, outs, fused, gamma,
+                                                   args.steps, args.warmup, flush)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    cells_per_rank = B * L * L
+    value = cells_per_rank * ws * args.steps / (max_ms / 1e3)
+
+    # ---- the other cost mode of the same config (same protocol) --------
+    other = None
+    if not args.single_mode:
+        o_ms, o_ph, _, o_peak = time_engine(eng, torch, x, y, outs, not fused, gamma,
+                                            args.steps, min(args.warmup, 3), flush)
+        t2 = torch.tensor([o_ms], device="cuda", dtype=torch.float64)
+        if ws > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        o_max = float(t2.item())
+        other = {"cost_mode": "unfused" if fused else "fused",
+                 "value": cells_per_rank * ws * args.steps / (o_max / 1e3), "unit": "cells/s",
+                 "ms_per_step": o_max / args.steps, "peak_hbm_mb": o_peak / 2**20,
+                 "phase_ms_per_step": {k: v / args.steps for k, v in o_ph.items()}}
+
+    # ---- e2e through the public API with pinned host buffers ----------
+    xh = x.cpu().pin_memory()
+    yh = y.cpu().pin_memory()
+    lh = torch.empty(B).pin_memory()
+    gxh = torch.empty((B, L, D)).pin_memory()
+    gyh = torch.empty((B, L, D)).pin_memory()
+    for _ in range(min(args.warmup, 2)):
+        eng.sdtw_with_gradients(xh, yh, gamma, fused=fused, out=(lh, gxh, gyh))
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        eng.sdtw_with_gradients(xh, yh, gamma, fused=fused, out=(lh, gxh, gyh))
+        e.record(stream)
+        e.synchronize()
+        e2e_ms += s.elapsed_time(e)
+    t3 = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t3, op=dist.ReduceOp.MAX)
+    e2e_max = float(t3.item())
+    h2d = 2 * B * L * D * 4
+    d2h = B * 4 + 2 * B * L * D * 4
+
+    # ---- roofline of the dominant kernel --------------------------------
+    peaks, src = _peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    mufu_peak = SM_COUNT * MUFU_PER_CLK_SM * sm_mhz * 1e6 / 1e9  # G MUFU op/s
+    per_step = {k: v / args.steps for k, v in phases.items()}
+    dom = max(per_step, key=per_step.get) if per_step else "backward"
+    roofline = None
+    if dom in ("forward", "backward"):
+        mufu = MUFU_FWD if dom == "forward" else MUFU_BWD
+        ach = mufu * cells_per_rank / (per_step[dom] / 1e3) / 1e9
+        roofline = {"bound": "sfu", "kernel": f"sdtw_{dom}_kernel", "achieved": ach,
+                    "peak": mufu_peak, "unit": "GMUFU-op/s", "frac": ach / mufu_peak,
+                    "traffic": _traffic(args, dom),
+                    "algorithmic": f"{mufu} MUFU/cell x {cells_per_rank} cells per launch "
+                                   "(SURVEY.md §8(d))",
+                    "peak_basis": f"{SM_COUNT} SM x {MUFU_PER_CLK_SM} MUFU/clk x {sm_mhz} MHz "
+                                  f"(sm_max_mhz, {src})",
+                    "share_of_step": per_step[dom] / (total_ms / args.steps)}
+    elif dom == "grads":
+        flop = 2 * 2 * cells_per_rank * D
+        ach = flop / (per_step[dom] / 1e3) / 1e12
+        pk = float(peaks.get("bf16_tflops", 1590.0))
+        roofline = {"bound": "tensor", "kernel": "grad_contract_kernel", "achieved": ach,
+                    "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
+                    "share_of_step": per_step[dom] / (total_ms / args.steps)}
+    elif dom == "costs":
+        byt = 4 * cells_per_rank
+        ach = byt / (per_step[dom] / 1e3) / 1e9
+        pk = float(peaks.get("hbm_gbs", 6650.0))
+        roofline = {"bound": "hbm", "kernel": "cost_skewed_kernel", "achieved": ach, "peak": pk,
+                    "unit": "GB/s", "frac": ach / pk, "traffic": None,
+                    "share_of_step": per_step[dom] / (total_ms / args.steps)}
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic N(0,1) (torch.randn, seed 42+rank), fp32",
+            "config": _config_dict(args, cfg, ws),
+            "peak_hbm_mb": peak / 2**20,
+            "phase_ms_per_step": per_step,
+            "e2e": {"value": cells_per_rank * ws * args.steps / (e2e_max / 1e3),
+                    "unit": "cells/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_max / args.steps},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "clocks": clk,
+        }
+        if other:
+            line["unfused" if fused else "fused"] = other
+        if ws == 1 and not args.no_cpu_baseline:
+            try:
+                pairs = _ref_pairs_for(cfg)
+                v, ms, sample = cpu_reference_rate(cfg, fused, os.cpu_count() or 1, 2, 1,
+                                                   max_pairs=pairs)
+                line["cpu_baseline"] = {"value": v, "unit": "cells/s",
+                                        "cores": os.cpu_count() or 1, "kind": "reference",
+                                        "sample": sample}
+            except Exception as exc:  # the baseline is reported, not required
+                line["cpu_baseline"] = {"value": None, "unit": "cells/s", "cores": 0,
+                                        "kind": "reference", "sample": f"unavailable: {exc}"}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
+def _traffic(args, dom):
+    """dram bytes per launch from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        return t.get(f"{args.config}_{args.mode}_{dom}")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="fused", choices=["fused", "unfused"])
+    ap.add_argument("--single-mode", action="store_true", help="skip the other cost mode")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_engine_arm(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

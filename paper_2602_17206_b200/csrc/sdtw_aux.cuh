@@ -1,0 +1,336 @@
+// sdtw_aux.cuh — norms, the unfused cost tensor, input-gradient contraction,
+// the padded-table kernels of the standalone API, and the Adam step.
+#pragma once
+#include "sdtw_common.cuh"
+#include "sdtw_dp.cuh"
+
+namespace sdtw {
+
+// NormCache (cost.hpp:22-56): one thread per row, sequential feature order.
+template <class T>
+__global__ void norms_kernel(const T *__restrict__ x, int rows, int D, T *__restrict__ out)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const T *e = x + (size_t)r * D;
+    T s = T(0);
+    for (int k = 0; k < D; ++k) s = fma(e[k], e[k], s);
+    out[r] = s;
+}
+
+// Unfused cost tensor (materialize_costs, cost.hpp:82-99) written directly in
+// the DP's skewed strip layout dsk[b][s][k][t] = d(32s+t+1, k-t+1), so the
+// forward and backward read one 128-byte line per warp step.
+template <class T>
+__global__ void cost_skewed_kernel(const T *__restrict__ x, const T *__restrict__ y,
+                                   const T *__restrict__ xn, const T *__restrict__ yn,
+                                   int B, int N, int M, int D, int S, int bw,
+                                   T *__restrict__ dsk)
+{
+    const size_t per_strip = (size_t)(M + 31) * 32;
+    const size_t total = (size_t)B * S * per_strip;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int t = (int)(idx & 31);
+        const size_t rest = idx >> 5;
+        const int kk = (int)(rest % (M + 31));
+        const size_t bs = rest / (M + 31);
+        const int s = (int)(bs % S), b = (int)(bs / S);
+        const int i = 32 * s + t + 1, j = kk - t + 1;
+        T v = T(0);
+        if (i <= N && j >= 1 && j <= M && in_band(i, j, bw))
+            v = cost_cell(x + ((size_t)b * N + (i - 1)) * D, y + ((size_t)b * M + (j - 1)) * D,
+                          xn[(size_t)b * N + (i - 1)], yn[(size_t)b * M + (j - 1)], D);
+        dsk[idx] = v;
+    }
+}
+
+// Row-major B x N x M costs (CostMatrixBatch layout) for the standalone API.
+template <class T>
+__global__ void cost_rowmajor_kernel(const T *__restrict__ x, const T *__restrict__ y,
+                                     const T *__restrict__ xn, const T *__restrict__ yn,
+                                     int B, int N, int M, int D, T *__restrict__ d)
+{
+    const size_t total = (size_t)B * N * M;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx % M);
+        const size_t r = idx / M;
+        const int i = (int)(r % N), b = (int)(r / N);
+        d[idx] = cost_cell(x + ((size_t)b * N + i) * D, y + ((size_t)b * M + j) * D,
+                           xn[(size_t)b * N + i], yn[(size_t)b * M + j], D);
+    }
+}
+
+// input_gradients (backward.hpp:208-266) as two batched contractions:
+//   out[b,p,:] = 2 (src[b,p,:] * sum_q W(p,q) - sum_q W(p,q) other[b,q,:])
+// with W = E (rows of E, p = i) or W = E^T (p = j).  E is dense B x N x M.
+// Tiled 32 x 32 outputs per block (32 x 8 threads, 4 outputs per thread).
+template <class T, bool kTransE>
+__global__ void __launch_bounds__(256) grad_contract_kernel(const T *__restrict__ E,
+                                                            const T *__restrict__ src,
+                                                            const T *__restrict__ other,
+                                                            int N, int M, int D,
+                                                            T *__restrict__ out)
+{
+    // P rows of the output, Q reduction length
+    const int P = kTransE ? M : N, Q = kTransE ? N : M;
+    const int b = blockIdx.z;
+    const int p0 = blockIdx.y * 32, f0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty in [0,8)
+    __shared__ T w_s[32][33];   // [p][q]
+    __shared__ T o_s[32][33];   // [q][f]
+    T acc[4] = {T(0), T(0), T(0), T(0)};
+    T marg[4] = {T(0), T(0), T(0), T(0)};
+    const T *Eb = E + (size_t)b * N * M;
+    const T *ob = other + (size_t)b * Q * D;
+    for (int q0 = 0; q0 < Q; q0 += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            if (kTransE) {  // W(p,q) = E(q,p): read E row q0+r, columns p0+tx
+                const int p = p0 + tx, q = q0 + r;
+                w_s[tx][r] = (p < P && q < Q) ? Eb[(size_t)q * M + p] : T(0);
+            } else {
+                const int p = p0 + r, q = q0 + tx;
+                w_s[r][tx] = (p < P && q < Q) ? Eb[(size_t)p * M + q] : T(0);
+            }
+            const int qq = q0 + r, f = f0 + tx;
+            o_s[r][tx] = (qq < Q && f < D) ? ob[(size_t)qq * D + f] : T(0);
+        }
+        __syncthreads();
+        for (int qi = 0; qi < 32; ++qi) {
+            const T ov = o_s[qi][tx];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const T wv = w_s[ty + 8 * u][qi];
+                acc[u] = fma(wv, ov, acc[u]);
+                marg[u] += wv;
+            }
+        }
+        __syncthreads();
+    }
+    const T *sb = src + (size_t)b * P * D;
+    T *obp = out + (size_t)b * P * D;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int p = p0 + ty + 8 * u, f = f0 + tx;
+        if (p < P && f < D) obp[(size_t)p * D + f] = T(2) * (sb[(size_t)p * D + f] * marg[u] - acc[u]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Padded-table kernels for the standalone API (CS3: forward -> R table ->
+// backward_log / backward_linear on a host-visible table).  One CTA per pair
+// walks anti-diagonals exactly as the reference sweep does
+// (wavefront.hpp:81-110, backward.hpp:29-177), evaluating the reference cell
+// formulas in T on the given table values.
+// ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ T ref_softmin(T a, T b, T c, T g)
+{
+    T mn = b < a ? b : a;
+    mn = c < mn ? c : mn;
+    if (isinf(mn)) return mn;
+    const T s = exp(-(a - mn) / g) + exp(-(b - mn) / g) + exp(-(c - mn) / g);
+    return mn - g * log(s);
+}
+template <class T>
+__device__ __forceinline__ T ref_lse3(T a, T b, T c)
+{
+    T m = a < b ? b : a;
+    m = m < c ? c : m;
+    if (isinf(m)) return m;
+    return m + log(exp(a - m) + exp(b - m) + exp(c - m));
+}
+
+// R table (double accumulation) from the row-major cost tensor.  Output in T.
+// forward.hpp:25-37 with R kept in double so the returned table is accurate
+// to the last bit of T.
+template <class T>
+__global__ void __launch_bounds__(1024) table_forward_kernel(const T *__restrict__ d, int N, int M,
+                                                             int bw, double gamma,
+                                                             double *__restrict__ Rw,
+                                                             T *__restrict__ R_out)
+{
+    const int b = blockIdx.x;
+    const size_t W = (size_t)M + 2, cells = (size_t)(N + 2) * W;
+    double *R = Rw + (size_t)b * cells;
+    const double inf = Num<double>::inf();
+    for (size_t c = threadIdx.x; c < cells; c += blockDim.x) R[c] = inf;
+    __syncthreads();
+    if (threadIdx.x == 0) R[0] = 0.0;
+    __syncthreads();
+    const T *db = d + (size_t)b * N * M;
+    for (int p = 0; p <= N + M - 2; ++p) {
+        const int lo = max(0, p - M + 1), hi = min(N - 1, p);
+        for (int ci = lo + threadIdx.x; ci <= hi; ci += blockDim.x) {
+            const int cj = p - ci;
+            if (!in_band(ci + 1, cj + 1, bw)) continue;
+            const int i = ci + 1, j = cj + 1;
+            const double sm = ref_softmin<double>(R[(i - 1) * W + j - 1], R[(i - 1) * W + j],
+                                                  R[i * W + j - 1], gamma);
+            R[i * W + j] = (double)db[(size_t)ci * M + cj] + sm;
+        }
+        __syncthreads();
+    }
+    T *Ro = R_out + (size_t)b * cells;
+    for (size_t c = threadIdx.x; c < cells; c += blockDim.x) Ro[c] = (T)R[c];
+}
+
+// backward_sweep<T, Cost, kLog> (backward.hpp:29-177) on a given R table.
+// Rin is read only (the reference stages it in a ring); E_out gets E.
+template <class T>
+__global__ void __launch_bounds__(1024) table_backward_kernel(const T *__restrict__ Rin,
+                                                              const T *__restrict__ d, int N, int M,
+                                                              int bw, T gamma, int log_space,
+                                                              T *__restrict__ Eo, int *incomplete)
+{
+    const int b = blockIdx.x;
+    const size_t W = (size_t)M + 2, cells = (size_t)(N + 2) * W;
+    const T *R = Rin + (size_t)b * cells;
+    T *E = Eo + (size_t)b * cells;
+    const T *db = d + (size_t)b * N * M;
+    const T inf = Num<T>::inf();
+    for (size_t c = threadIdx.x; c < cells; c += blockDim.x) E[c] = inf;
+    __syncthreads();
+    auto cost = [&](int i, int j) { return db[(size_t)(i - 1) * M + (j - 1)]; };
+    for (int p = N + M - 2; p >= 0; --p) {
+        const int lo = max(0, p - M + 1), hi = min(N - 1, p);
+        for (int ci = lo + threadIdx.x; ci <= hi; ci += blockDim.x) {
+            const int cj = p - ci;
+            if (!in_band(ci + 1, cj + 1, bw)) continue;
+            const int i = ci + 1, j = cj + 1;
+            if (ci == N - 1 && cj == M - 1) {
+                E[i * W + j] = log_space ? T(0) : T(1);
+                continue;
+            }
+            const T r_self = R[i * W + j];
+            if (isinf(r_self)) {
+                *incomplete = 1;
+                continue;
+            }
+            T down = -inf, right = -inf, diag = -inf;
+            if (ci + 1 < N) {
+                const T rs = in_band(i + 1, j, bw) ? R[(i + 1) * W + j] : inf;
+                if (!isinf(rs)) down = (rs - r_self - cost(i + 1, j)) / gamma;
+            }
+            if (cj + 1 < M) {
+                const T rs = in_band(i, j + 1, bw) ? R[i * W + j + 1] : inf;
+                if (!isinf(rs)) right = (rs - r_self - cost(i, j + 1)) / gamma;
+            }
+            if (ci + 1 < N && cj + 1 < M) {
+                const T rs = in_band(i + 1, j + 1, bw) ? R[(i + 1) * W + j + 1] : inf;
+                if (!isinf(rs)) diag = (rs - r_self - cost(i + 1, j + 1)) / gamma;
+            }
+            if (log_space) {
+                const T td = isinf(down) ? -inf : E[(i + 1) * W + j] + down;
+                const T tr = isinf(right) ? -inf : E[i * W + j + 1] + right;
+                const T tg = isinf(diag) ? -inf : E[(i + 1) * W + j + 1] + diag;
+                const T l = ref_lse3<T>(td, tr, tg);
+                E[i * W + j] = l < T(0) ? l : T(0);
+            } else {
+                T acc = T(0);
+                if (!isinf(down)) acc += exp(down) * E[(i + 1) * W + j];
+                if (!isinf(right)) acc += exp(right) * E[i * W + j + 1];
+                if (!isinf(diag)) acc += exp(diag) * E[(i + 1) * W + j + 1];
+                E[i * W + j] = acc;
+            }
+        }
+        __syncthreads();
+    }
+    // epilogue (backward.hpp:161-174)
+    for (size_t c = threadIdx.x; c < cells; c += blockDim.x) {
+        const int i = (int)(c / W), j = (int)(c % W);
+        const bool interior = i >= 1 && i <= N && j >= 1 && j <= M && in_band(i, j, bw);
+        T v = E[c];
+        if (!interior) v = T(0);
+        else if (log_space) v = exp(v);
+        E[c] = v;
+    }
+}
+
+// Dense E (B x N x M) -> padded E table (B x (N+2) x (M+2)), zero border.
+template <class T>
+__global__ void pad_table_kernel(const T *__restrict__ E, int B, int N, int M,
+                                 T *__restrict__ Et)
+{
+    const size_t W = (size_t)M + 2, cells = (size_t)(N + 2) * W;
+    const size_t total = (size_t)B * cells;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = idx / cells, c = idx % cells;
+        const int i = (int)(c / W), j = (int)(c % W);
+        T v = T(0);
+        if (i >= 1 && i <= N && j >= 1 && j <= M) v = E[(b * N + (i - 1)) * M + (j - 1)];
+        Et[idx] = v;
+    }
+}
+
+// Padded E table -> dense E.
+template <class T>
+__global__ void unpad_table_kernel(const T *__restrict__ Et, int B, int N, int M,
+                                   T *__restrict__ E)
+{
+    const size_t total = (size_t)B * N * M;
+    const size_t W = (size_t)M + 2, cells = (size_t)(N + 2) * W;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t b = idx / ((size_t)N * M), r = idx % ((size_t)N * M);
+        const int i = (int)(r / M), j = (int)(r % M);
+        E[idx] = Et[b * cells + (size_t)(i + 1) * W + (j + 1)];
+    }
+}
+
+// Barycenter: members are pairs (z, x_k); broadcast z into the x batch.
+template <class T>
+__global__ void broadcast_kernel(const T *__restrict__ z, size_t n, int K, T *__restrict__ out)
+{
+    const size_t total = n * (size_t)K;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x)
+        out[idx] = z[idx % n];
+}
+
+// Weighted member reduction in fixed member order (barycenter.hpp:75-84):
+// value = sum_k w_k loss_k (double), grad[i] = sum_k T(w_k) grad_x[k][i].
+template <class T>
+__global__ void member_reduce_kernel(const T *__restrict__ gx, const T *__restrict__ loss,
+                                     const double *__restrict__ w, int K, size_t n,
+                                     T *__restrict__ grad, double *value)
+{
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        T acc = T(0);
+        for (int k = 0; k < K; ++k) {
+            const double wk = w ? w[k] : 1.0;
+            if (wk == 0.0) continue;
+            acc += (T)wk * gx[(size_t)k * n + i];
+        }
+        grad[i] = acc;
+    }
+    if (i == 0 && value) {
+        double v = 0.0;
+        for (int k = 0; k < K; ++k) {
+            const double wk = w ? w[k] : 1.0;
+            if (wk == 0.0) continue;
+            v += wk * (double)loss[k];
+        }
+        *value = v;
+    }
+}
+
+// Adam with fp64 moments (barycenter.hpp:181-191).
+template <class T>
+__global__ void adam_kernel(T *__restrict__ z, const T *__restrict__ g, double *__restrict__ m1,
+                            double *__restrict__ m2, size_t n, double bc1, double bc2,
+                            double lr, double b1, double b2, double eps)
+{
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double gi = (double)g[i];
+    m1[i] = b1 * m1[i] + (1.0 - b1) * gi;
+    m2[i] = b2 * m2[i] + (1.0 - b2) * gi * gi;
+    const double step = lr * (m1[i] / bc1) / (sqrt(m2[i] / bc2) + eps);
+    z[i] -= (T)step;
+}
+
+}  // namespace sdtw

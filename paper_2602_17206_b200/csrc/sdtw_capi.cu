@@ -1,0 +1,997 @@
+// sdtw_capi.cu — host side of the C-ABI (include/sdtw_capi.h).
+//
+// Owns: the per-context device allocator with the reference's ledger
+// semantics (live / peak / limit -> OutOfMemoryError, types.hpp:60-88), the
+// stream, host<->device staging, validation in the reference's order
+// (forward.hpp:48-53, types.hpp:230-243), launch orchestration of the
+// kernels in sdtw_dp.cuh / sdtw_aux.cuh, and the NCCL communicator of the
+// multi-GPU barycenter.  No CPU fallback: every numeric result comes from a
+// device kernel.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/sdtw_capi.h"
+#include "sdtw_aux.cuh"
+#include "sdtw_common.cuh"
+#include "sdtw_dp.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local size_t g_oom_bytes = 0;
+
+struct SdtwError {
+    int code;
+    std::string msg;
+    size_t bytes;
+};
+
+[[noreturn]] void fail(int code, const std::string &msg, size_t bytes = 0)
+{
+    throw SdtwError{code, msg, bytes};
+}
+
+#define CUDA_OK(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            fail(SDTW_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+    } while (0)
+
+// --------------------------------------------------------------------------
+// Device allocator: exact-size caching, ledger accounting on live bytes.
+// --------------------------------------------------------------------------
+struct Allocator {
+    std::multimap<size_t, void *> cache;
+    std::unordered_map<void *, size_t> live;
+    size_t live_bytes = 0, peak_bytes = 0, limit_bytes = 0;
+
+    static size_t round(size_t b) { return b < 512 ? 512 : (b + 511) & ~size_t(511); }
+
+    void *alloc(size_t bytes)
+    {
+        const size_t sz = round(bytes);
+        if (limit_bytes != 0 && live_bytes + sz > limit_bytes) fail(SDTW_ENOMEM, "device ledger limit", sz);
+        void *p = nullptr;
+        auto it = cache.find(sz);
+        if (it != cache.end()) {
+            p = it->second;
+            cache.erase(it);
+        } else {
+            if (cudaMalloc(&p, sz) != cudaSuccess) {
+                cudaGetLastError();
+                trim();
+                if (cudaMalloc(&p, sz) != cudaSuccess) {
+                    cudaGetLastError();
+                    fail(SDTW_ENOMEM, "cudaMalloc failed", sz);
+                }
+            }
+        }
+        live[p] = sz;
+        live_bytes += sz;
+        peak_bytes = std::max(peak_bytes, live_bytes);
+        return p;
+    }
+    void release(void *p)
+    {
+        if (!p) return;
+        auto it = live.find(p);
+        if (it == live.end()) return;
+        live_bytes -= it->second;
+        cache.emplace(it->second, p);
+        live.erase(it);
+    }
+    void trim()
+    {
+        for (auto &kv : cache) cudaFree(kv.second);
+        cache.clear();
+    }
+};
+
+// dlopen'ed NCCL (shares the process's libnccl.so.2, e.g. torch's copy).
+struct Nccl {
+    typedef int (*GetUid)(void *);
+    typedef int (*InitRank)(void **, int, const void *uid_by_value_dummy, int);
+    void *lib = nullptr;
+    void *get_uid = nullptr, *init_rank = nullptr, *allreduce = nullptr, *destroy = nullptr,
+         *err_str = nullptr;
+    bool load()
+    {
+        if (lib) return true;
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) return false;
+        get_uid = dlsym(lib, "ncclGetUniqueId");
+        init_rank = dlsym(lib, "ncclCommInitRank");
+        allreduce = dlsym(lib, "ncclAllReduce");
+        destroy = dlsym(lib, "ncclCommDestroy");
+        err_str = dlsym(lib, "ncclGetErrorString");
+        return get_uid && init_rank && allreduce && destroy;
+    }
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+struct NcclUid {
+    char internal[128];
+};
+
+}  // namespace
+
+struct sdtw_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    Allocator alloc;
+    uint64_t launches = 0;
+    int sm_count = 148;
+    void *nccl_comm = nullptr;
+    int nranks = 1, rank = 0;
+    bool timing = false;
+    cudaEvent_t ev[SDTW_NUM_PHASES][2] = {};
+    bool ev_used[SDTW_NUM_PHASES] = {};
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// RAII device buffer from the context allocator.
+template <class T>
+struct Buf {
+    sdtw_ctx *ctx = nullptr;
+    T *p = nullptr;
+    size_t n = 0;
+    Buf() = default;
+    Buf(sdtw_ctx *c, size_t count) : ctx(c), n(count)
+    {
+        p = count ? static_cast<T *>(c->alloc.alloc(count * sizeof(T))) : nullptr;
+    }
+    Buf(const Buf &) = delete;
+    Buf &operator=(const Buf &) = delete;
+    Buf(Buf &&o) noexcept : ctx(o.ctx), p(o.p), n(o.n) { o.p = nullptr; }
+    Buf &operator=(Buf &&o) noexcept
+    {
+        if (this != &o) {
+            if (p) ctx->alloc.release(p);
+            ctx = o.ctx;
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+        }
+        return *this;
+    }
+    ~Buf()
+    {
+        if (p) ctx->alloc.release(p);
+    }
+};
+
+// Input view: either the caller's device pointer or a staged device copy.
+template <class T>
+struct In {
+    Buf<T> owned;
+    const T *p = nullptr;
+    In(sdtw_ctx *c, const T *src, size_t count, bool host)
+    {
+        if (!src || count == 0) return;
+        if (host) {
+            owned = Buf<T>(c, count);
+            CUDA_OK(cudaMemcpyAsync(owned.p, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+            p = owned.p;
+        } else {
+            p = src;
+        }
+    }
+};
+
+// Output view: device scratch copied back to the host at finish().
+template <class T>
+struct Out {
+    Buf<T> owned;
+    T *p = nullptr;
+    T *user = nullptr;
+    size_t n = 0;
+    bool host = false;
+    Out(sdtw_ctx *c, T *dst, size_t count, bool h) : user(dst), n(count), host(h)
+    {
+        if (!dst || count == 0) return;
+        if (host) {
+            owned = Buf<T>(c, count);
+            p = owned.p;
+        } else {
+            p = dst;
+        }
+    }
+    void finish(sdtw_ctx *c)
+    {
+        if (host && user)
+            CUDA_OK(cudaMemcpyAsync(user, p, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    }
+};
+
+#define LAUNCH(ctx, kernel, grid, block, smem, ...)                         \
+    do {                                                                    \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);    \
+        ++(ctx)->launches;                                                  \
+        CUDA_OK(cudaGetLastError());                                        \
+    } while (0)
+
+// Brackets one pipeline phase with events when timing is enabled.
+struct Phase {
+    sdtw_ctx *ctx;
+    int id;
+    Phase(sdtw_ctx *c, int i) : ctx(c), id(i)
+    {
+        if (ctx->timing) {
+            cudaEventRecord(ctx->ev[id][0], ctx->stream);
+            ctx->ev_used[id] = true;
+        }
+    }
+    ~Phase()
+    {
+        if (ctx->timing) cudaEventRecord(ctx->ev[id][1], ctx->stream);
+    }
+};
+
+void reset_phases(sdtw_ctx *ctx)
+{
+    for (int i = 0; i < SDTW_NUM_PHASES; ++i) ctx->ev_used[i] = false;
+}
+
+unsigned grid_for(size_t total, unsigned block, unsigned cap = 148u * 64u)
+{
+    size_t g = (total + block - 1) / block;
+    if (g == 0) g = 1;
+    return (unsigned)std::min<size_t>(g, cap);
+}
+
+template <class Fn>
+int guarded(sdtw_ctx *ctx, Fn &&fn)
+{
+    try {
+        if (!ctx) fail(SDTW_EINVAL, "null context");
+        DeviceGuard dg(ctx->device);
+        fn();
+        return SDTW_OK;
+    } catch (const SdtwError &e) {
+        g_err = e.msg;
+        g_oom_bytes = e.bytes;
+        return e.code;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return SDTW_ECUDA;
+    }
+}
+
+// A dependency wait that gave up means a scheduling bug: surface it.
+void check_wait_timeouts()
+{
+    int n = 0;
+    CUDA_OK(cudaMemcpyFromSymbol(&n, sdtw::g_sdtw_wait_timeouts, sizeof(int)));
+    if (n != 0) {
+        const int zero = 0;
+        cudaMemcpyToSymbol(sdtw::g_sdtw_wait_timeouts, &zero, sizeof(int));
+        fail(SDTW_ECUDA, "internal: " + std::to_string(n) + " wavefront dependency wait(s) timed out");
+    }
+}
+
+void finish_call(sdtw_ctx *ctx, int ptr_kind)
+{
+    if (!(ptr_kind & SDTW_FLAG_ASYNC)) {
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        check_wait_timeouts();
+    }
+}
+
+// validate_config (types.hpp:230-243) + forward's shape checks
+// (forward.hpp:48-53), in the reference's order.
+void validate(size_t B, size_t N, size_t M, size_t D, const sdtw_config *cfg)
+{
+    if (!cfg) fail(SDTW_EINVAL, "null config");
+    if (B == 0 || N == 0 || M == 0 || D == 0) fail(SDTW_EINVAL, "series batch dimensions must be >= 1");
+    if (!(cfg->gamma > 0.0)) fail(SDTW_EINVAL, "gamma must be > 0 (got " + std::to_string(cfg->gamma) + ")");
+    const size_t gap = N > M ? N - M : M - N;
+    if (cfg->bandwidth != 0 && cfg->bandwidth < gap)
+        fail(SDTW_EINVAL, "bandwidth " + std::to_string(cfg->bandwidth) + " < |N - M| = " +
+                              std::to_string(gap) + ": end cell unreachable");
+    if (cfg->normalized && N != M) fail(SDTW_EINVAL, "normalized sdtw requires N == M");
+    if (N > (1u << 30) || M > (1u << 30) || D > (1u << 20)) fail(SDTW_EINVAL, "dimension too large");
+}
+
+// --------------------------------------------------------------------------
+// The fused forward+backward pipeline on device pointers.
+// --------------------------------------------------------------------------
+template <class T>
+struct Pipeline {
+    sdtw_ctx *ctx;
+    int B, N, M, D, S, C, bw;
+    bool fused;
+    double gamma;
+    const T *x, *y;
+    Buf<T> xn, yn, dsk, hb, vc, sb, E;
+    Buf<double> lpart;
+    Buf<int> flags;  // 2*B*S flags + 2 tickets
+
+    Pipeline(sdtw_ctx *c, const T *xd, const T *yd, size_t B_, size_t N_, size_t M_, size_t D_,
+             const sdtw_config *cfg)
+        : ctx(c), B((int)B_), N((int)N_), M((int)M_), D((int)D_), bw((int)cfg->bandwidth),
+          fused(cfg->cost_mode == SDTW_COST_FUSED), gamma(cfg->gamma), x(xd), y(yd)
+    {
+        S = (N + 31) / 32;
+        C = (M + 31) / 32;
+    }
+
+    sdtw::DpArgs<T> args()
+    {
+        sdtw::DpArgs<T> a{};
+        a.B = B; a.N = N; a.M = M; a.D = D; a.S = S; a.C = C; a.bw = bw;
+        const T g = (T)gamma;  // gamma cast to T first (forward.hpp:62)
+        a.k = (T)(1.4426950408889634 / (double)g);
+        a.gln2 = (T)((double)g * 0.6931471805599453);
+        a.dsk = dsk.p; a.x = x; a.y = y; a.xn = xn.p; a.yn = yn.p;
+        a.hb = hb.p; a.vc = vc.p; a.sb = sb.p; a.lpart = lpart.p; a.E = E.p;
+        a.flag_f = flags.p; a.flag_b = flags.p + (size_t)B * S;
+        a.tickets = reinterpret_cast<unsigned *>(flags.p + 2 * (size_t)B * S);
+        return a;
+    }
+
+    int dp_grid() const
+    {
+        const int warps = B * S;
+        return std::max(1, std::min(warps, ctx->sm_count * 32));
+    }
+
+    void norms()
+    {
+        reset_phases(ctx);
+        Phase ph(ctx, 0);
+        xn = Buf<T>(ctx, (size_t)B * N);
+        yn = Buf<T>(ctx, (size_t)B * M);
+        LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * N, 128), 128, 0, x, B * N, D, xn.p);
+        LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * M, 128), 128, 0, y, B * M, D, yn.p);
+    }
+
+    void costs()
+    {
+        if (fused) return;
+        Phase ph(ctx, 1);
+        const size_t total = (size_t)B * S * (M + 31) * 32;
+        dsk = Buf<T>(ctx, total);
+        LAUNCH(ctx, sdtw::cost_skewed_kernel<T>, grid_for(total, 256), 256, 0, x, y, xn.p, yn.p, B,
+               N, M, D, S, bw, dsk.p);
+    }
+
+    // loss_f / loss_d: device outputs (either may be null)
+    void forward(float *loss_f, double *loss_d)
+    {
+        hb = Buf<T>(ctx, (size_t)B * S * M);
+        vc = Buf<T>(ctx, (size_t)B * C * N);
+        lpart = Buf<double>(ctx, (size_t)B * S);
+        flags = Buf<int>(ctx, 2 * (size_t)B * S + 2);
+        CUDA_OK(cudaMemsetAsync(flags.p, 0, flags.n * sizeof(int), ctx->stream));
+        auto a = args();
+        Phase ph(ctx, 2);
+        if (fused)
+            LAUNCH(ctx, (sdtw::sdtw_forward_kernel<T, true>), dp_grid(), 32, 0, a);
+        else
+            LAUNCH(ctx, (sdtw::sdtw_forward_kernel<T, false>), dp_grid(), 32, 0, a);
+        LAUNCH(ctx, sdtw::sdtw_loss_reduce_kernel, grid_for(B, 128), 128, 0, lpart.p, B, S, loss_f,
+               loss_d);
+    }
+
+    void backward()
+    {
+        sb = Buf<T>(ctx, (size_t)B * S * M);
+        E = Buf<T>(ctx, (size_t)B * N * M);
+        auto a = args();
+        Phase ph(ctx, 3);
+        if (fused)
+            LAUNCH(ctx, (sdtw::sdtw_backward_kernel<T, true>), dp_grid(), 32, 0, a);
+        else
+            LAUNCH(ctx, (sdtw::sdtw_backward_kernel<T, false>), dp_grid(), 32, 0, a);
+        // the cost tensor is dropped after the backward (backward.hpp:291)
+        dsk = Buf<T>();
+    }
+
+    void grads(T *gx, T *gy)
+    {
+        Phase ph(ctx, 4);
+        if (gx) {
+            dim3 grid((D + 31) / 32, (N + 31) / 32, B);
+            LAUNCH(ctx, (sdtw::grad_contract_kernel<T, false>), grid, 256, 0, E.p, x, y, N, M, D, gx);
+        }
+        if (gy) {
+            dim3 grid((D + 31) / 32, (M + 31) / 32, B);
+            LAUNCH(ctx, (sdtw::grad_contract_kernel<T, true>), grid, 256, 0, E.p, y, x, N, M, D, gy);
+        }
+    }
+};
+
+template <class T>
+void loss_out(Pipeline<T> &pl, T *loss_dev);
+template <>
+void loss_out<float>(Pipeline<float> &pl, float *loss_dev) { pl.forward(loss_dev, nullptr); }
+template <>
+void loss_out<double>(Pipeline<double> &pl, double *loss_dev) { pl.forward(nullptr, loss_dev); }
+
+template <class T>
+void check_finite_loss(sdtw_ctx *ctx, const T *loss_dev, size_t B)
+{
+    std::vector<T> h(B);
+    CUDA_OK(cudaMemcpyAsync(h.data(), loss_dev, B * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    for (size_t b = 0; b < B; ++b)
+        if (!std::isfinite((double)h[b]))
+            fail(SDTW_EUNREACHABLE, "forward: R[N,M] is not finite (end cell unreachable)");
+}
+
+template <class T>
+int fwd_bwd(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_t M, size_t D,
+            const sdtw_config *cfg, int ptr_kind, T *loss, T *gx, T *gy)
+{
+    return guarded(ctx, [&] {
+        validate(B, N, M, D, cfg);
+        if (!loss) fail(SDTW_EINVAL, "loss output is required");
+        const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
+        In<T> xi(ctx, x, B * N * D, host), yi(ctx, y, B * M * D, host);
+        Out<T> lo(ctx, loss, B, host), gxo(ctx, gx, B * N * D, host), gyo(ctx, gy, B * M * D, host);
+        if (cfg->backward_space == SDTW_BWD_LINEAR) {
+            fail(SDTW_EINVAL, "linear-space backward is served by sdtw_backward_table_*");
+        }
+        Pipeline<T> pl(ctx, xi.p, yi.p, B, N, M, D, cfg);
+        pl.norms();
+        pl.costs();
+        loss_out<T>(pl, lo.p);
+        pl.backward();
+        pl.grads(gxo.p, gyo.p);
+        lo.finish(ctx);
+        gxo.finish(ctx);
+        gyo.finish(ctx);
+        finish_call(ctx, ptr_kind);
+    });
+}
+
+template <class T>
+int forward_backward_E(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_t M,
+                       size_t D, const sdtw_config *cfg, int ptr_kind, T *loss, T *E_out)
+{
+    return guarded(ctx, [&] {
+        validate(B, N, M, D, cfg);
+        const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
+        In<T> xi(ctx, x, B * N * D, host), yi(ctx, y, B * M * D, host);
+        Out<T> lo(ctx, loss, B, host);
+        Out<T> eo(ctx, E_out, B * (N + 2) * (M + 2), host);
+        Buf<T> ltmp;
+        T *ldev = lo.p;
+        if (!ldev) {
+            ltmp = Buf<T>(ctx, B);
+            ldev = ltmp.p;
+        }
+        Pipeline<T> pl(ctx, xi.p, yi.p, B, N, M, D, cfg);
+        pl.norms();
+        pl.costs();
+        loss_out<T>(pl, ldev);
+        pl.backward();
+        if (eo.p) {
+            const size_t total = B * (N + 2) * (M + 2);
+            LAUNCH(ctx, sdtw::pad_table_kernel<T>, grid_for(total, 256), 256, 0, pl.E.p, (int)B,
+                   (int)N, (int)M, eo.p);
+        }
+        lo.finish(ctx);
+        eo.finish(ctx);
+        finish_call(ctx, ptr_kind);
+    });
+}
+
+template <class T>
+int forward_api(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_t M, size_t D,
+                const sdtw_config *cfg, int ptr_kind, T *loss, T *R_out, T *costs_out,
+                T *norms_out)
+{
+    return guarded(ctx, [&] {
+        validate(B, N, M, D, cfg);
+        const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
+        In<T> xi(ctx, x, B * N * D, host), yi(ctx, y, B * M * D, host);
+        Out<T> lo(ctx, loss, B, host);
+        Out<T> ro(ctx, R_out, B * (N + 2) * (M + 2), host);
+        Out<T> co(ctx, costs_out, B * N * M, host);
+        Out<T> no(ctx, norms_out, B * (N + M), host);
+        Buf<T> ltmp;
+        T *ldev = lo.p;
+        if (!ldev) {
+            ltmp = Buf<T>(ctx, B);
+            ldev = ltmp.p;
+        }
+        Pipeline<T> pl(ctx, xi.p, yi.p, B, N, M, D, cfg);
+        pl.norms();
+        pl.costs();
+        loss_out<T>(pl, ldev);
+        if (no.p) {
+            CUDA_OK(cudaMemcpyAsync(no.p, pl.xn.p, B * N * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+            CUDA_OK(cudaMemcpyAsync(no.p + B * N, pl.yn.p, B * M * sizeof(T), cudaMemcpyDeviceToDevice,
+                                    ctx->stream));
+        }
+        if (ro.p || co.p) {
+            Buf<T> dtmp;
+            T *d = co.p;
+            if (!d) {
+                dtmp = Buf<T>(ctx, B * N * M);
+                d = dtmp.p;
+            }
+            LAUNCH(ctx, sdtw::cost_rowmajor_kernel<T>, grid_for(B * N * M, 256), 256, 0, xi.p, yi.p,
+                   pl.xn.p, pl.yn.p, (int)B, (int)N, (int)M, (int)D, d);
+            if (ro.p) {
+                Buf<double> rw(ctx, B * (N + 2) * (M + 2));
+                LAUNCH(ctx, sdtw::table_forward_kernel<T>, (unsigned)B, 1024, 0, d, (int)N, (int)M,
+                       (int)cfg->bandwidth, (double)(T)cfg->gamma, rw.p, ro.p);
+            }
+        }
+        lo.finish(ctx);
+        ro.finish(ctx);
+        co.finish(ctx);
+        no.finish(ctx);
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        check_finite_loss<T>(ctx, ldev, B);
+    });
+}
+
+template <class T>
+int backward_table(sdtw_ctx *ctx, const T *R, const T *costs, const T *x, const T *y, size_t B,
+                   size_t N, size_t M, size_t D, const sdtw_config *cfg, int ptr_kind, T *E_out)
+{
+    return guarded(ctx, [&] {
+        if (!cfg) fail(SDTW_EINVAL, "null config");
+        if (B == 0 || N == 0 || M == 0) fail(SDTW_EINVAL, "dp table dimensions must be >= 1");
+        sdtw_config c2 = *cfg;
+        validate(B, N, M, D == 0 ? 1 : D, &c2);
+        if (!R || !E_out) fail(SDTW_EINVAL, "R and E_out are required");
+        const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
+        const size_t cells = B * (N + 2) * (M + 2);
+        In<T> ri(ctx, R, cells, host);
+        Out<T> eo(ctx, E_out, cells, host);
+        Buf<T> dtmp;
+        const T *d = nullptr;
+        In<T> ci(ctx, costs, B * N * M, host);
+        if (costs) {
+            d = ci.p;
+        } else {
+            if (!x || !y || D == 0) fail(SDTW_EINVAL, "costs or x/y required");
+            In<T> xi(ctx, x, B * N * D, host), yi(ctx, y, B * M * D, host);
+            Buf<T> xn(ctx, B * N), yn(ctx, B * M);
+            LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for(B * N, 128), 128, 0, xi.p, (int)(B * N), (int)D, xn.p);
+            LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for(B * M, 128), 128, 0, yi.p, (int)(B * M), (int)D, yn.p);
+            dtmp = Buf<T>(ctx, B * N * M);
+            LAUNCH(ctx, sdtw::cost_rowmajor_kernel<T>, grid_for(B * N * M, 256), 256, 0, xi.p, yi.p,
+                   xn.p, yn.p, (int)B, (int)N, (int)M, (int)D, dtmp.p);
+            d = dtmp.p;
+            CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        }
+        Buf<int> inc(ctx, 1);
+        CUDA_OK(cudaMemsetAsync(inc.p, 0, sizeof(int), ctx->stream));
+        LAUNCH(ctx, sdtw::table_backward_kernel<T>, (unsigned)B, 1024, 0, ri.p, d, (int)N, (int)M,
+               (int)cfg->bandwidth, (T)cfg->gamma, cfg->backward_space == SDTW_BWD_LOG ? 1 : 0, eo.p,
+               inc.p);
+        int h_inc = 0;
+        CUDA_OK(cudaMemcpyAsync(&h_inc, inc.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        if (h_inc) fail(SDTW_EINCOMPLETE, "backward: forward table has +inf at a reachable in-band cell");
+        eo.finish(ctx);
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+template <class T>
+int input_grads(sdtw_ctx *ctx, const T *E, const T *x, const T *y, size_t B, size_t N, size_t M,
+                size_t D, int ptr_kind, T *gx, T *gy)
+{
+    return guarded(ctx, [&] {
+        if (B == 0 || N == 0 || M == 0 || D == 0) fail(SDTW_EINVAL, "input_gradients: shape mismatch");
+        const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
+        const size_t cells = B * (N + 2) * (M + 2);
+        In<T> ei(ctx, E, cells, host), xi(ctx, x, B * N * D, host), yi(ctx, y, B * M * D, host);
+        Out<T> gxo(ctx, gx, B * N * D, host), gyo(ctx, gy, B * M * D, host);
+        Buf<T> dense(ctx, B * N * M);
+        LAUNCH(ctx, sdtw::unpad_table_kernel<T>, grid_for(B * N * M, 256), 256, 0, ei.p, (int)B,
+               (int)N, (int)M, dense.p);
+        if (gxo.p) {
+            dim3 grid((unsigned)((D + 31) / 32), (unsigned)((N + 31) / 32), (unsigned)B);
+            LAUNCH(ctx, (sdtw::grad_contract_kernel<T, false>), grid, 256, 0, dense.p, xi.p, yi.p,
+                   (int)N, (int)M, (int)D, gxo.p);
+        }
+        if (gyo.p) {
+            dim3 grid((unsigned)((D + 31) / 32), (unsigned)((M + 31) / 32), (unsigned)B);
+            LAUNCH(ctx, (sdtw::grad_contract_kernel<T, true>), grid, 256, 0, dense.p, yi.p, xi.p,
+                   (int)N, (int)M, (int)D, gyo.p);
+        }
+        gxo.finish(ctx);
+        gyo.finish(ctx);
+        finish_call(ctx, ptr_kind);
+    });
+}
+
+// barycenter_objective (barycenter.hpp:60-86): all members in one batch.
+template <class T>
+int bary_objective(sdtw_ctx *ctx, const T *z, size_t Lz, const T *members, size_t K, size_t L,
+                   size_t D, double gamma, size_t bw, const double *weights, int ptr_kind,
+                   double *value, T *grad)
+{
+    return guarded(ctx, [&] {
+        if (K == 0) fail(SDTW_EINVAL, "barycenter: need at least one member series");
+        if (Lz == 0) fail(SDTW_EINVAL, "barycenter: target length must be >= 1");
+        if (weights) {
+            double sum = 0;
+            for (size_t k = 0; k < K; ++k) {
+                if (weights[k] < 0) fail(SDTW_EINVAL, "barycenter: negative weight");
+                sum += weights[k];
+            }
+            if (sum == 0) fail(SDTW_EINVAL, "barycenter: all weights are zero");
+        }
+        sdtw_config cfg{gamma, bw, SDTW_COST_UNFUSED, SDTW_BWD_LOG, 0};
+        validate(K, Lz, L, D, &cfg);
+        const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
+        In<T> zi(ctx, z, Lz * D, host), mi(ctx, members, K * L * D, host);
+        Out<T> go(ctx, grad, Lz * D, host);
+        Out<double> vo(ctx, value, 1, host);
+        Buf<double> wd;
+        if (weights) {
+            wd = Buf<double>(ctx, K);
+            CUDA_OK(cudaMemcpyAsync(wd.p, weights, K * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        Buf<T> zb(ctx, K * Lz * D);
+        LAUNCH(ctx, sdtw::broadcast_kernel<T>, grid_for(K * Lz * D, 256), 256, 0, zi.p, Lz * D,
+               (int)K, zb.p);
+        Buf<T> loss(ctx, K), gx(ctx, K * Lz * D);
+        Pipeline<T> pl(ctx, zb.p, mi.p, K, Lz, L, D, &cfg);
+        pl.norms();
+        pl.costs();
+        loss_out<T>(pl, loss.p);
+        pl.backward();
+        pl.grads(gx.p, nullptr);
+        LAUNCH(ctx, sdtw::member_reduce_kernel<T>, grid_for(Lz * D, 256), 256, 0, gx.p, loss.p,
+               wd.p, (int)K, Lz * D, go.p, vo.p);
+        go.finish(ctx);
+        vo.finish(ctx);
+        finish_call(ctx, ptr_kind);
+    });
+}
+
+template <class T>
+int adam_step(sdtw_ctx *ctx, T *z, const T *grad, double *m1, double *m2, size_t n, size_t t,
+              double lr, double b1, double b2, double eps, int ptr_kind)
+{
+    return guarded(ctx, [&] {
+        if (t == 0) fail(SDTW_EINVAL, "adam: iteration index is 1-based");
+        const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
+        const double bc1 = 1.0 - std::pow(b1, double(t)), bc2 = 1.0 - std::pow(b2, double(t));
+        In<T> gi(ctx, grad, n, host);
+        Buf<T> zt;
+        Buf<double> m1t, m2t;
+        T *zd = z;
+        double *m1d = m1, *m2d = m2;
+        if (host) {
+            zt = Buf<T>(ctx, n);
+            m1t = Buf<double>(ctx, n);
+            m2t = Buf<double>(ctx, n);
+            CUDA_OK(cudaMemcpyAsync(zt.p, z, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+            CUDA_OK(cudaMemcpyAsync(m1t.p, m1, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            CUDA_OK(cudaMemcpyAsync(m2t.p, m2, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            zd = zt.p;
+            m1d = m1t.p;
+            m2d = m2t.p;
+        }
+        LAUNCH(ctx, sdtw::adam_kernel<T>, grid_for(n, 256), 256, 0, zd, gi.p, m1d, m2d, n, bc1, bc2,
+               lr, b1, b2, eps);
+        if (host) {
+            CUDA_OK(cudaMemcpyAsync(z, zd, n * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_OK(cudaMemcpyAsync(m1, m1d, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_OK(cudaMemcpyAsync(m2, m2d, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        finish_call(ctx, ptr_kind);
+    });
+}
+
+}  // namespace
+
+// ============================================================================
+// extern "C"
+// ============================================================================
+extern "C" {
+
+int sdtw_ctx_create(int device, sdtw_ctx **out)
+{
+    if (!out) return SDTW_EINVAL;
+    try {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            g_err = "no CUDA device available (the engine has no CPU fallback)";
+            return SDTW_ECUDA;
+        }
+        if (device < 0 || device >= n) {
+            g_err = "device index out of range";
+            return SDTW_EINVAL;
+        }
+        auto *ctx = new sdtw_ctx();
+        ctx->device = device;
+        DeviceGuard dg(device);
+        cudaDeviceProp prop{};
+        CUDA_OK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) {
+            delete ctx;
+            g_err = "the engine is built for sm_100a (B200); found sm_" + std::to_string(prop.major) +
+                    std::to_string(prop.minor);
+            return SDTW_ECUDA;
+        }
+        ctx->sm_count = prop.multiProcessorCount;
+        CUDA_OK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+        ctx->stream = ctx->own_stream;
+        *out = ctx;
+        return SDTW_OK;
+    } catch (const SdtwError &e) {
+        g_err = e.msg;
+        return e.code;
+    }
+}
+
+int sdtw_ctx_destroy(sdtw_ctx *ctx)
+{
+    if (!ctx) return SDTW_OK;
+    {
+        DeviceGuard dg(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->nccl_comm && g_nccl.destroy) ((int (*)(void *))g_nccl.destroy)(ctx->nccl_comm);
+        for (auto &kv : ctx->alloc.live) cudaFree(kv.first);
+        ctx->alloc.trim();
+        if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    }
+    delete ctx;
+    return SDTW_OK;
+}
+
+int sdtw_ctx_set_stream(sdtw_ctx *ctx, void *stream)
+{
+    if (!ctx) return SDTW_EINVAL;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return SDTW_OK;
+}
+
+void *sdtw_ctx_stream(sdtw_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int sdtw_ctx_synchronize(sdtw_ctx *ctx)
+{
+    return guarded(ctx, [&] { CUDA_OK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int sdtw_mem_stats(sdtw_ctx *ctx, size_t *live, size_t *peak)
+{
+    if (!ctx) return SDTW_EINVAL;
+    if (live) *live = ctx->alloc.live_bytes;
+    if (peak) *peak = ctx->alloc.peak_bytes;
+    return SDTW_OK;
+}
+
+int sdtw_mem_reset_peak(sdtw_ctx *ctx)
+{
+    if (!ctx) return SDTW_EINVAL;
+    ctx->alloc.peak_bytes = ctx->alloc.live_bytes;
+    return SDTW_OK;
+}
+
+int sdtw_set_mem_limit(sdtw_ctx *ctx, size_t limit)
+{
+    if (!ctx) return SDTW_EINVAL;
+    ctx->alloc.limit_bytes = limit;
+    return SDTW_OK;
+}
+
+int sdtw_mem_trim(sdtw_ctx *ctx)
+{
+    return guarded(ctx, [&] {
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        ctx->alloc.trim();
+    });
+}
+
+uint64_t sdtw_launch_count(sdtw_ctx *ctx) { return ctx ? ctx->launches : 0; }
+void sdtw_reset_launch_count(sdtw_ctx *ctx)
+{
+    if (ctx) ctx->launches = 0;
+}
+
+int sdtw_ctx_enable_timing(sdtw_ctx *ctx, int enable)
+{
+    return guarded(ctx, [&] {
+        if (enable && !ctx->timing) {
+            for (int i = 0; i < SDTW_NUM_PHASES; ++i)
+                for (int k = 0; k < 2; ++k)
+                    if (!ctx->ev[i][k]) CUDA_OK(cudaEventCreate(&ctx->ev[i][k]));
+        }
+        ctx->timing = enable != 0;
+        reset_phases(ctx);
+    });
+}
+
+int sdtw_phase_times(sdtw_ctx *ctx, float *ms, int n)
+{
+    return guarded(ctx, [&] {
+        for (int i = 0; i < n && i < SDTW_NUM_PHASES; ++i) {
+            ms[i] = -1.0f;
+            if (ctx->timing && ctx->ev_used[i]) {
+                CUDA_OK(cudaEventSynchronize(ctx->ev[i][1]));
+                CUDA_OK(cudaEventElapsedTime(&ms[i], ctx->ev[i][0], ctx->ev[i][1]));
+            }
+        }
+    });
+}
+
+const char *sdtw_last_error(void) { return g_err.c_str(); }
+size_t sdtw_last_oom_bytes(void) { return g_oom_bytes; }
+
+int sdtw_fwd_bwd_f32(sdtw_ctx *ctx, const float *x, const float *y, size_t B, size_t N, size_t M,
+                     size_t D, const sdtw_config *cfg, int ptr_kind, float *loss, float *gx, float *gy)
+{
+    return fwd_bwd<float>(ctx, x, y, B, N, M, D, cfg, ptr_kind, loss, gx, gy);
+}
+int sdtw_fwd_bwd_f64(sdtw_ctx *ctx, const double *x, const double *y, size_t B, size_t N,
+                     size_t M, size_t D, const sdtw_config *cfg, int ptr_kind, double *loss,
+                     double *gx, double *gy)
+{
+    return fwd_bwd<double>(ctx, x, y, B, N, M, D, cfg, ptr_kind, loss, gx, gy);
+}
+
+int sdtw_forward_f32(sdtw_ctx *ctx, const float *x, const float *y, size_t B, size_t N, size_t M,
+                     size_t D, const sdtw_config *cfg, int ptr_kind, float *loss, float *R_out,
+                     float *costs_out, float *norms_out)
+{
+    return forward_api<float>(ctx, x, y, B, N, M, D, cfg, ptr_kind, loss, R_out, costs_out, norms_out);
+}
+int sdtw_forward_f64(sdtw_ctx *ctx, const double *x, const double *y, size_t B, size_t N,
+                     size_t M, size_t D, const sdtw_config *cfg, int ptr_kind, double *loss,
+                     double *R_out, double *costs_out, double *norms_out)
+{
+    return forward_api<double>(ctx, x, y, B, N, M, D, cfg, ptr_kind, loss, R_out, costs_out, norms_out);
+}
+
+int sdtw_backward_table_f32(sdtw_ctx *ctx, const float *R, const float *costs, const float *x,
+                            const float *y, size_t B, size_t N, size_t M, size_t D,
+                            const sdtw_config *cfg, int ptr_kind, float *E_out)
+{
+    return backward_table<float>(ctx, R, costs, x, y, B, N, M, D, cfg, ptr_kind, E_out);
+}
+int sdtw_backward_table_f64(sdtw_ctx *ctx, const double *R, const double *costs, const double *x,
+                            const double *y, size_t B, size_t N, size_t M, size_t D,
+                            const sdtw_config *cfg, int ptr_kind, double *E_out)
+{
+    return backward_table<double>(ctx, R, costs, x, y, B, N, M, D, cfg, ptr_kind, E_out);
+}
+
+int sdtw_forward_backward_E_f32(sdtw_ctx *ctx, const float *x, const float *y, size_t B, size_t N,
+                                size_t M, size_t D, const sdtw_config *cfg, int ptr_kind,
+                                float *loss, float *E_out)
+{
+    return forward_backward_E<float>(ctx, x, y, B, N, M, D, cfg, ptr_kind, loss, E_out);
+}
+int sdtw_forward_backward_E_f64(sdtw_ctx *ctx, const double *x, const double *y, size_t B,
+                                size_t N, size_t M, size_t D, const sdtw_config *cfg,
+                                int ptr_kind, double *loss, double *E_out)
+{
+    return forward_backward_E<double>(ctx, x, y, B, N, M, D, cfg, ptr_kind, loss, E_out);
+}
+
+int sdtw_input_grads_f32(sdtw_ctx *ctx, const float *E, const float *x, const float *y, size_t B,
+                         size_t N, size_t M, size_t D, int ptr_kind, float *gx, float *gy)
+{
+    return input_grads<float>(ctx, E, x, y, B, N, M, D, ptr_kind, gx, gy);
+}
+int sdtw_input_grads_f64(sdtw_ctx *ctx, const double *E, const double *x, const double *y,
+                         size_t B, size_t N, size_t M, size_t D, int ptr_kind, double *gx,
+                         double *gy)
+{
+    return input_grads<double>(ctx, E, x, y, B, N, M, D, ptr_kind, gx, gy);
+}
+
+int sdtw_barycenter_objective_f32(sdtw_ctx *ctx, const float *z, size_t Lz, const float *members,
+                                  size_t K, size_t L, size_t D, double gamma, size_t bandwidth,
+                                  const double *weights, int ptr_kind, double *value, float *grad)
+{
+    return bary_objective<float>(ctx, z, Lz, members, K, L, D, gamma, bandwidth, weights, ptr_kind,
+                                 value, grad);
+}
+int sdtw_barycenter_objective_f64(sdtw_ctx *ctx, const double *z, size_t Lz,
+                                  const double *members, size_t K, size_t L, size_t D,
+                                  double gamma, size_t bandwidth, const double *weights,
+                                  int ptr_kind, double *value, double *grad)
+{
+    return bary_objective<double>(ctx, z, Lz, members, K, L, D, gamma, bandwidth, weights, ptr_kind,
+                                  value, grad);
+}
+
+int sdtw_adam_step_f32(sdtw_ctx *ctx, float *z, const float *grad, double *m1, double *m2, size_t n,
+                       size_t t, double lr, double b1, double b2, double eps, int ptr_kind)
+{
+    return adam_step<float>(ctx, z, grad, m1, m2, n, t, lr, b1, b2, eps, ptr_kind);
+}
+int sdtw_adam_step_f64(sdtw_ctx *ctx, double *z, const double *grad, double *m1, double *m2,
+                       size_t n, size_t t, double lr, double b1, double b2, double eps,
+                       int ptr_kind)
+{
+    return adam_step<double>(ctx, z, grad, m1, m2, n, t, lr, b1, b2, eps, ptr_kind);
+}
+
+// ---- NCCL (barycenter gradient allreduce) ---------------------------------
+int sdtw_nccl_get_unique_id(void *uid128)
+{
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (!uid128) return SDTW_EINVAL;
+    if (!g_nccl.load()) {
+        g_err = "libnccl.so.2 not loadable";
+        return SDTW_ENCCL;
+    }
+    int rc = ((int (*)(NcclUid *))g_nccl.get_uid)(static_cast<NcclUid *>(uid128));
+    if (rc != 0) {
+        g_err = "ncclGetUniqueId failed";
+        return SDTW_ENCCL;
+    }
+    return SDTW_OK;
+}
+
+int sdtw_nccl_init(sdtw_ctx *ctx, const void *uid128, int nranks, int rank)
+{
+    return guarded(ctx, [&] {
+        std::lock_guard<std::mutex> lk(g_nccl_mu);
+        if (!uid128 || nranks < 1 || rank < 0 || rank >= nranks) fail(SDTW_EINVAL, "bad nccl args");
+        if (!g_nccl.load()) fail(SDTW_ENCCL, "libnccl.so.2 not loadable");
+        NcclUid uid;
+        std::memcpy(&uid, uid128, sizeof uid);
+        void *comm = nullptr;
+        int rc = ((int (*)(void **, int, NcclUid, int))g_nccl.init_rank)(&comm, nranks, uid, rank);
+        if (rc != 0) fail(SDTW_ENCCL, "ncclCommInitRank failed: " + std::to_string(rc));
+        ctx->nccl_comm = comm;
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+    });
+}
+
+int sdtw_nccl_finalize(sdtw_ctx *ctx)
+{
+    return guarded(ctx, [&] {
+        if (ctx->nccl_comm && g_nccl.destroy) ((int (*)(void *))g_nccl.destroy)(ctx->nccl_comm);
+        ctx->nccl_comm = nullptr;
+    });
+}
+
+int sdtw_allreduce_grad_f32(sdtw_ctx *ctx, float *grad, size_t n, double *value)
+{
+    return guarded(ctx, [&] {
+        if (!ctx->nccl_comm) fail(SDTW_ENCCL, "nccl not initialised on this context");
+        // ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0 (nccl.h)
+        typedef int (*AR)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+        AR ar = (AR)g_nccl.allreduce;
+        int rc = ar(grad, grad, n, 7, 0, ctx->nccl_comm, ctx->stream);
+        if (rc == 0 && value) rc = ar(value, value, 1, 8, 0, ctx->nccl_comm, ctx->stream);
+        if (rc != 0) fail(SDTW_ENCCL, "ncclAllReduce failed: " + std::to_string(rc));
+    });
+}
+
+}  // extern "C"
