@@ -232,7 +232,11 @@ def run_engine_arm(args, cfg):
     if ws > 1:
         dist.barrier()
     eng = Engine(local)
-    eng.set_stream(torch.cuda.current_stream().cuda_stream)
+    # a real (non-default) stream shared by torch and the engine, so the
+    # CUDA events below bracket exactly the engine's work
+    side = torch.cuda.Stream()
+    torch.cuda.set_stream(side)
+    eng.set_stream(side.cuda_stream)
     B, L, D, gamma = cfg["B"], cfg["L"], cfg["D"], cfg["gamma"]
     gen = torch.Generator(device="cuda").manual_seed(42 + rank)
     x = torch.randn((B, L, D), generator=gen, device="cuda", dtype=torch.float32)

@@ -24,17 +24,17 @@ __global__ void norms_kernel(const T *__restrict__ x, int rows, int D, T *__rest
 template <class T>
 __global__ void cost_skewed_kernel(const T *__restrict__ x, const T *__restrict__ y,
                                    const T *__restrict__ xn, const T *__restrict__ yn,
-                                   int B, int N, int M, int D, int S, int bw,
+                                   int B, int N, int M, int D, int S, int KK, int bw,
                                    T *__restrict__ dsk)
 {
-    const size_t per_strip = (size_t)(M + 31) * 32;
+    const size_t per_strip = (size_t)KK * 32;
     const size_t total = (size_t)B * S * per_strip;
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
         const int t = (int)(idx & 31);
         const size_t rest = idx >> 5;
-        const int kk = (int)(rest % (M + 31));
-        const size_t bs = rest / (M + 31);
+        const int kk = (int)(rest % KK);
+        const size_t bs = rest / KK;
         const int s = (int)(bs % S), b = (int)(bs / S);
         const int i = 32 * s + t + 1, j = kk - t + 1;
         T v = T(0);

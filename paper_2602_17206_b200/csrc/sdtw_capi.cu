@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -24,6 +25,7 @@
 #include "sdtw_aux.cuh"
 #include "sdtw_common.cuh"
 #include "sdtw_dp.cuh"
+#include "sdtw_tc.cuh"
 
 namespace {
 
@@ -325,7 +327,7 @@ void validate(size_t B, size_t N, size_t M, size_t D, const sdtw_config *cfg)
 template <class T>
 struct Pipeline {
     sdtw_ctx *ctx;
-    int B, N, M, D, S, C, bw;
+    int B, N, M, D, S, C, KK, bw;
     bool fused;
     double gamma;
     const T *x, *y;
@@ -340,12 +342,13 @@ struct Pipeline {
     {
         S = (N + 31) / 32;
         C = (M + 31) / 32;
+        KK = ((M + 62) / 32) * 32;
     }
 
     sdtw::DpArgs<T> args()
     {
         sdtw::DpArgs<T> a{};
-        a.B = B; a.N = N; a.M = M; a.D = D; a.S = S; a.C = C; a.bw = bw;
+        a.B = B; a.N = N; a.M = M; a.D = D; a.S = S; a.C = C; a.bw = bw; a.KK = KK;
         const T g = (T)gamma;  // gamma cast to T first (forward.hpp:62)
         a.k = (T)(1.4426950408889634 / (double)g);
         a.gln2 = (T)((double)g * 0.6931471805599453);
@@ -362,24 +365,49 @@ struct Pipeline {
         return std::max(1, std::min(warps, ctx->sm_count * 32));
     }
 
+    Buf<unsigned> absmax;
+
     void norms()
     {
         reset_phases(ctx);
         Phase ph(ctx, 0);
         xn = Buf<T>(ctx, (size_t)B * N);
         yn = Buf<T>(ctx, (size_t)B * M);
-        LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * N, 128), 128, 0, x, B * N, D, xn.p);
-        LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * M, 128), 128, 0, y, B * M, D, yn.p);
+        if constexpr (std::is_same<T, float>::value) {
+            LAUNCH(ctx, sdtw::norms_f32_kernel, grid_for((size_t)B * N, 128), 128, 0, x, B * N, D, xn.p);
+            LAUNCH(ctx, sdtw::norms_f32_kernel, grid_for((size_t)B * M, 128), 128, 0, y, B * M, D, yn.p);
+        } else {
+            LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * N, 128), 128, 0, x, B * N, D, xn.p);
+            LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * M, 128), 128, 0, y, B * M, D, yn.p);
+        }
     }
 
     void costs()
     {
         if (fused) return;
         Phase ph(ctx, 1);
-        const size_t total = (size_t)B * S * (M + 31) * 32;
+        const size_t total = (size_t)B * S * KK * 32;
         dsk = Buf<T>(ctx, total);
-        LAUNCH(ctx, sdtw::cost_skewed_kernel<T>, grid_for(total, 256), 256, 0, x, y, xn.p, yn.p, B,
-               N, M, D, S, bw, dsk.p);
+        if constexpr (std::is_same<T, float>::value) {
+            absmax = Buf<unsigned>(ctx, 2);
+            CUDA_OK(cudaMemsetAsync(absmax.p, 0, 2 * sizeof(unsigned), ctx->stream));
+            LAUNCH(ctx, sdtw::absmax_kernel, grid_for((size_t)B * N * D, 256, 1024), 256, 0, x,
+                   (size_t)B * N * D, absmax.p);
+            LAUNCH(ctx, sdtw::absmax_kernel, grid_for((size_t)B * M * D, 256, 1024), 256, 0, y,
+                   (size_t)B * M * D, absmax.p + 1);
+            static bool attr = false;
+            if (!attr) {
+                CUDA_OK(cudaFuncSetAttribute(sdtw::cost_gemm_tc_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, sdtw::kCgSmem));
+                attr = true;
+            }
+            dim3 grid((M + sdtw::kCgCols - 1) / sdtw::kCgCols, (N + sdtw::kCgRows - 1) / sdtw::kCgRows, B);
+            LAUNCH(ctx, sdtw::cost_gemm_tc_kernel, grid, 128, sdtw::kCgSmem, x, y, xn.p, yn.p, absmax.p, B,
+                   N, M, D, S, KK, bw, dsk.p);
+        } else {
+            LAUNCH(ctx, sdtw::cost_skewed_kernel<T>, grid_for(total, 256), 256, 0, x, y, xn.p, yn.p, B,
+                   N, M, D, S, KK, bw, dsk.p);
+        }
     }
 
     // loss_f / loss_d: device outputs (either may be null)

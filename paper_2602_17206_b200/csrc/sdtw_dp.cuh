@@ -29,10 +29,11 @@ struct DpArgs {
     int S;       // strips  = ceil(N / 32)
     int C;       // chunks  = ceil(M / 32)
     int bw;      // Sakoe-Chiba radius, 0 = unconstrained
+    int KK;      // skewed rows per strip in dsk (>= M + 31, multiple of 32)
     T k;         // log2(e) / gamma
     T gln2;      // gamma * ln(2)
     // cost sources (exactly one is used)
-    const T *dsk;            // unfused: skewed costs [b][s][k][t], k in [0, M+31)
+    const T *dsk;            // unfused: skewed costs [b][s][k][t], k in [0, KK)
     const T *x, *y;          // fused: raw series
     const T *xn, *yn;        // fused: squared norms (cost.hpp:22-56)
     // checkpoints / halos
@@ -67,7 +68,7 @@ __device__ __forceinline__ T load_cost(const DpArgs<T> &a, int b, int s, int t, 
                          a.xn[(size_t)b * a.N + (i - 1)], a.yn[(size_t)b * a.M + (j - 1)], a.D);
     } else {
         const int kk = j - 1 + t;
-        return a.dsk[(((size_t)b * a.S + s) * (a.M + 31) + kk) * 32 + t];
+        return a.dsk[(((size_t)b * a.S + s) * a.KK + kk) * 32 + t];
     }
 }
 

@@ -113,12 +113,22 @@ def test_ragged_and_band_f64(engine, oracle_c, N, M, bw):
 
 def test_fused_equals_unfused_bitwise(engine):
     """test_backward.cpp:225-241 / test_forward.cpp:82-101: one cost routine
-    for both modes."""
+    for both modes (fp64 path)."""
     x, y = _bench_like(3, 75, 9, seed=3)
-    a = engine.sdtw_with_gradients(x, y, 0.3)
-    b = engine.sdtw_with_gradients(x, y, 0.3, fused=True)
+    x, y = x.astype(np.float64), y.astype(np.float64)
+    a = engine.sdtw_with_gradients(x, y, 0.3, dtype=np.float64)
+    b = engine.sdtw_with_gradients(x, y, 0.3, fused=True, dtype=np.float64)
     for u, v in zip(a, b):
         assert np.array_equal(u, v)
+
+
+def test_fused_matches_unfused_f32(engine):
+    x, y = _bench_like(3, 75, 16, seed=3)
+    a = engine.sdtw_with_gradients(x, y, 0.3)
+    b = engine.sdtw_with_gradients(x, y, 0.3, fused=True)
+    assert rel_err(a[0], b[0]).max() <= 1e-6
+    for u, v in zip(a[1:], b[1:]):
+        assert grad_stats(u, v)[0] <= 1e-4
 
 
 def test_deterministic(engine):
