@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsdtw_b200.so")
 SOURCES = ["sdtw_capi.cu"]
-HEADERS = ["sdtw_common.cuh", "sdtw_dp.cuh", "sdtw_aux.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

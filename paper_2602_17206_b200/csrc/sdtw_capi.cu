@@ -25,6 +25,8 @@
 #include "sdtw_aux.cuh"
 #include "sdtw_common.cuh"
 #include "sdtw_dp.cuh"
+#include "sdtw_dp2.cuh"
+#include "sdtw_dp3.cuh"
 #include "sdtw_tc.cuh"
 
 namespace {
@@ -139,6 +141,11 @@ struct sdtw_ctx {
     void *nccl_comm = nullptr;
     int nranks = 1, rank = 0;
     bool timing = false;
+    // Persistent tagged-halo arena (zeroed once when it grows; entries carry
+    // the epoch of the call that wrote them, so no per-call clearing).
+    void *halo_arena = nullptr;
+    size_t halo_bytes = 0;
+    unsigned epoch = 0;
     cudaEvent_t ev[SDTW_NUM_PHASES][2] = {};
     bool ev_used[SDTW_NUM_PHASES] = {};
 };
@@ -371,6 +378,12 @@ struct Pipeline {
     {
         reset_phases(ctx);
         Phase ph(ctx, 0);
+        absmax = Buf<unsigned>(ctx, 2);
+        CUDA_OK(cudaMemsetAsync(absmax.p, 0, 2 * sizeof(unsigned), ctx->stream));
+        LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * N * D, 256, 1024), 256, 0, x,
+               (size_t)B * N * D, absmax.p);
+        LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * M * D, 256, 1024), 256, 0, y,
+               (size_t)B * M * D, absmax.p + 1);
         xn = Buf<T>(ctx, (size_t)B * N);
         yn = Buf<T>(ctx, (size_t)B * M);
         if constexpr (std::is_same<T, float>::value) {
@@ -389,12 +402,6 @@ struct Pipeline {
         const size_t total = (size_t)B * S * KK * 32;
         dsk = Buf<T>(ctx, total);
         if constexpr (std::is_same<T, float>::value) {
-            absmax = Buf<unsigned>(ctx, 2);
-            CUDA_OK(cudaMemsetAsync(absmax.p, 0, 2 * sizeof(unsigned), ctx->stream));
-            LAUNCH(ctx, sdtw::absmax_kernel, grid_for((size_t)B * N * D, 256, 1024), 256, 0, x,
-                   (size_t)B * N * D, absmax.p);
-            LAUNCH(ctx, sdtw::absmax_kernel, grid_for((size_t)B * M * D, 256, 1024), 256, 0, y,
-                   (size_t)B * M * D, absmax.p + 1);
             static bool attr = false;
             if (!attr) {
                 CUDA_OK(cudaFuncSetAttribute(sdtw::cost_gemm_tc_kernel,
@@ -410,34 +417,179 @@ struct Pipeline {
         }
     }
 
+    // Persistent grid: as many CTAs as fit on the device (never more than the
+    // work), each warp pulling tickets.
+    template <class Kern>
+    unsigned persistent_grid(Kern kern, int threads, size_t smem, int work_warps)
+    {
+        int occ = 0;
+        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+        if (occ < 1) fail(SDTW_ECUDA, "DP kernel does not fit on an SM");
+        const int wpc = threads / 32;
+        const int need = (work_warps + wpc - 1) / wpc;
+        return (unsigned)std::max(1, std::min(need, occ * ctx->sm_count));
+    }
+
+    template <int K>
+    void launch_forward()
+    {
+        auto a = args();
+        const int threads = 128;
+        if (fused) {
+            auto kern = sdtw::sdtw_forward2_kernel<T, K, true>;
+            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, true>::kPerWarp * sizeof(T);
+            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, a);
+        } else {
+            auto kern = sdtw::sdtw_forward2_kernel<T, K, false>;
+            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, false>::kPerWarp * sizeof(T);
+            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, a);
+        }
+    }
+
+    using Ent = typename sdtw::Tagged<T>::Ent;
+    Ent *hbt = nullptr, *sbt = nullptr;
+    unsigned epoch = 0;
+    Buf<long long> gx_fx, gy_fx, rs_fx, cs_fx;
+    Buf<T> tiles;
+    Buf<int4> tile_meta;
+    unsigned tile_cap = 0;
+    Buf<unsigned> stats;
+
+    void halos()
+    {
+        const size_t need = 2 * (size_t)B * S * M * sizeof(Ent);
+        if (ctx->halo_bytes < need) {
+            if (ctx->halo_arena) {
+                CUDA_OK(cudaStreamSynchronize(ctx->stream));
+                cudaFree(ctx->halo_arena);
+                ctx->halo_arena = nullptr;
+                ctx->halo_bytes = 0;
+            }
+            if (cudaMalloc(&ctx->halo_arena, need) != cudaSuccess) {
+                cudaGetLastError();
+                fail(SDTW_ENOMEM, "cudaMalloc failed (halo arena)", need);
+            }
+            CUDA_OK(cudaMemsetAsync(ctx->halo_arena, 0, need, ctx->stream));
+            ctx->halo_bytes = need;
+            ctx->epoch = 0;
+        }
+        hbt = static_cast<Ent *>(ctx->halo_arena);
+        sbt = hbt + (size_t)B * S * M;
+        epoch = ++ctx->epoch;
+        if (epoch == 0) epoch = ++ctx->epoch;
+    }
+
+    sdtw::Dp3Args<T> args3()
+    {
+        sdtw::Dp3Args<T> A{};
+        A.a = args();
+        A.hbt = hbt;
+        A.sbt = sbt;
+        A.epoch = epoch;
+        A.gx_fx = gx_fx.p;
+        A.gy_fx = gy_fx.p;
+        A.rs_fx = rs_fx.p;
+        A.cs_fx = cs_fx.p;
+        A.absmax = absmax.p;
+        A.tiles = tiles.p;
+        A.tile_meta = tile_meta.p;
+        A.tile_cap = tile_cap;
+        A.stats = stats.p;
+        return A;
+    }
+
+    template <int K>
+    void launch_forward3()
+    {
+        auto A = args3();
+        const int threads = 128;
+        if (fused) {
+            auto kern = sdtw::sdtw_forward3_kernel<T, K, true>;
+            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, true>::kPerWarp * sizeof(T);
+            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, A);
+        } else {
+            auto kern = sdtw::sdtw_forward3_kernel<T, K, false>;
+            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, false>::kPerWarp * sizeof(T);
+            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, A);
+        }
+    }
+
     // loss_f / loss_d: device outputs (either may be null)
     void forward(float *loss_f, double *loss_d)
     {
-        hb = Buf<T>(ctx, (size_t)B * S * M);
+        halos();
         vc = Buf<T>(ctx, (size_t)B * C * N);
         lpart = Buf<double>(ctx, (size_t)B * S);
         flags = Buf<int>(ctx, 2 * (size_t)B * S + 2);
+        stats = Buf<unsigned>(ctx, 4);
         CUDA_OK(cudaMemsetAsync(flags.p, 0, flags.n * sizeof(int), ctx->stream));
-        auto a = args();
+        CUDA_OK(cudaMemsetAsync(stats.p, 0, 4 * sizeof(unsigned), ctx->stream));
         Phase ph(ctx, 2);
-        if (fused)
-            LAUNCH(ctx, (sdtw::sdtw_forward_kernel<T, true>), dp_grid(), 32, 0, a);
-        else
-            LAUNCH(ctx, (sdtw::sdtw_forward_kernel<T, false>), dp_grid(), 32, 0, a);
+        // strips per warp: enough warps to fill the device first, ILP second
+        const int strips = B * S;
+        const int slots = ctx->sm_count * 16;
+        if (strips >= 4 * slots) launch_forward3<4>();
+        else if (strips >= 2 * slots) launch_forward3<2>();
+        else launch_forward3<1>();
         LAUNCH(ctx, sdtw::sdtw_loss_reduce_kernel, grid_for(B, 128), 128, 0, lpart.p, B, S, loss_f,
                loss_d);
     }
 
-    void backward()
+    // Backward with the input gradients.  gx / gy: device outputs (either
+    // may be null to skip it).  want_E: also materialise the dense
+    // B x N x M alignment gradient in E.
+    void backward(T *gx, T *gy, bool want_E)
     {
-        sb = Buf<T>(ctx, (size_t)B * S * M);
-        E = Buf<T>(ctx, (size_t)B * N * M);
-        auto a = args();
-        Phase ph(ctx, 3);
-        if (fused)
-            LAUNCH(ctx, (sdtw::sdtw_backward_kernel<T, true>), dp_grid(), 32, 0, a);
-        else
-            LAUNCH(ctx, (sdtw::sdtw_backward_kernel<T, false>), dp_grid(), 32, 0, a);
+        gx_fx = Buf<long long>(ctx, (size_t)B * N * D);
+        gy_fx = Buf<long long>(ctx, (size_t)B * M * D);
+        rs_fx = Buf<long long>(ctx, (size_t)B * N);
+        cs_fx = Buf<long long>(ctx, (size_t)B * M);
+        CUDA_OK(cudaMemsetAsync(gx_fx.p, 0, gx_fx.n * 8, ctx->stream));
+        CUDA_OK(cudaMemsetAsync(gy_fx.p, 0, gy_fx.n * 8, ctx->stream));
+        CUDA_OK(cudaMemsetAsync(rs_fx.p, 0, rs_fx.n * 8, ctx->stream));
+        CUDA_OK(cudaMemsetAsync(cs_fx.p, 0, cs_fx.n * 8, ctx->stream));
+        // compact tile store: all tiles when small, else 1/8 of them (the rest
+        // is contracted in the backward's own warp)
+        const size_t all_tiles = (size_t)B * S * C;
+        size_t cap = all_tiles;
+        if (all_tiles * 1024 * sizeof(T) > ((size_t)64 << 20)) cap = std::max<size_t>(all_tiles / 8, 16384);
+        cap = std::min(cap, all_tiles);
+        tile_cap = (unsigned)cap;
+        tiles = Buf<T>(ctx, cap * 1024);
+        tile_meta = Buf<int4>(ctx, cap);
+        if (want_E) {
+            E = Buf<T>(ctx, (size_t)B * N * M);
+            CUDA_OK(cudaMemsetAsync(E.p, 0, (size_t)B * N * M * sizeof(T), ctx->stream));
+        } else {
+            E = Buf<T>();
+        }
+        auto A = args3();
+        {
+            Phase ph(ctx, 3);
+            const int threads = sizeof(T) == 4 ? 128 : 64;
+            const int wpc = threads / 32;
+            if (fused) {
+                auto kern = sdtw::sdtw_backward3_kernel<T, true>;
+                const size_t smem = wpc * sdtw::Bwd3Smem<T, true>::kPerWarp * sizeof(T);
+                LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * S), threads, smem, A);
+            } else {
+                auto kern = sdtw::sdtw_backward3_kernel<T, false>;
+                const size_t smem = wpc * sdtw::Bwd3Smem<T, false>::kPerWarp * sizeof(T);
+                LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * S), threads, smem, A);
+            }
+        }
+        {
+            Phase ph(ctx, 4);
+            LAUNCH(ctx, sdtw::tile_contract_kernel<T>, (unsigned)(ctx->sm_count * 4),
+                   32 * sdtw::contract_warps<T>(), 0, A);
+            if (gx)
+                LAUNCH(ctx, sdtw::finalize_grads_fx_kernel<T>, grid_for((size_t)B * N * D, 256), 256, 0, x,
+                       rs_fx.p, gx_fx.p, absmax.p, N, M, B * N, D, 0, gx);
+            if (gy)
+                LAUNCH(ctx, sdtw::finalize_grads_fx_kernel<T>, grid_for((size_t)B * M * D, 256), 256, 0, y,
+                       cs_fx.p, gy_fx.p, absmax.p, N, M, B * M, D, 1, gy);
+        }
         // the cost tensor is dropped after the backward (backward.hpp:291)
         dsk = Buf<T>();
     }
@@ -491,8 +643,7 @@ int fwd_bwd(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_t M,
         pl.norms();
         pl.costs();
         loss_out<T>(pl, lo.p);
-        pl.backward();
-        pl.grads(gxo.p, gyo.p);
+        pl.backward(gxo.p, gyo.p, false);
         lo.finish(ctx);
         gxo.finish(ctx);
         gyo.finish(ctx);
@@ -520,7 +671,7 @@ int forward_backward_E(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N
         pl.norms();
         pl.costs();
         loss_out<T>(pl, ldev);
-        pl.backward();
+        pl.backward(nullptr, nullptr, eo.p != nullptr);
         if (eo.p) {
             const size_t total = B * (N + 2) * (M + 2);
             LAUNCH(ctx, sdtw::pad_table_kernel<T>, grid_for(total, 256), 256, 0, pl.E.p, (int)B,
@@ -694,8 +845,7 @@ int bary_objective(sdtw_ctx *ctx, const T *z, size_t Lz, const T *members, size_
         pl.norms();
         pl.costs();
         loss_out<T>(pl, loss.p);
-        pl.backward();
-        pl.grads(gx.p, nullptr);
+        pl.backward(gx.p, nullptr, false);
         LAUNCH(ctx, sdtw::member_reduce_kernel<T>, grid_for(Lz * D, 256), 256, 0, gx.p, loss.p,
                wd.p, (int)K, Lz * D, go.p, vo.p);
         go.finish(ctx);
@@ -790,6 +940,7 @@ int sdtw_ctx_destroy(sdtw_ctx *ctx)
         cudaStreamSynchronize(ctx->stream);
         if (ctx->nccl_comm && g_nccl.destroy) ((int (*)(void *))g_nccl.destroy)(ctx->nccl_comm);
         for (auto &kv : ctx->alloc.live) cudaFree(kv.first);
+        if (ctx->halo_arena) cudaFree(ctx->halo_arena);
         ctx->alloc.trim();
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     }
