@@ -93,6 +93,10 @@ void sdtw_reset_launch_count(sdtw_ctx *ctx);
 int sdtw_ctx_enable_timing(sdtw_ctx *ctx, int enable);
 int sdtw_phase_times(sdtw_ctx *ctx, float *ms, int n);
 
+/* Diagnostics: when trace_dev (device, 2 * B * S uint64) is non-NULL, the
+ * forward DP records %globaltimer at each strip's start and end. */
+int sdtw_debug_set_trace(sdtw_ctx *ctx, void *trace_dev);
+
 const char *sdtw_last_error(void);
 size_t sdtw_last_oom_bytes(void);
 

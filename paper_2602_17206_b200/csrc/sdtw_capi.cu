@@ -146,6 +146,7 @@ struct sdtw_ctx {
     void *halo_arena = nullptr;
     size_t halo_bytes = 0;
     unsigned epoch = 0;
+    unsigned long long *trace = nullptr;  // debug: per-strip forward timestamps
     cudaEvent_t ev[SDTW_NUM_PHASES][2] = {};
     bool ev_used[SDTW_NUM_PHASES] = {};
 };
@@ -496,6 +497,7 @@ struct Pipeline {
         A.tile_meta = tile_meta.p;
         A.tile_cap = tile_cap;
         A.stats = stats.p;
+        A.trace = ctx->trace;
         return A;
     }
 
@@ -1022,6 +1024,13 @@ int sdtw_phase_times(sdtw_ctx *ctx, float *ms, int n)
             }
         }
     });
+}
+
+int sdtw_debug_set_trace(sdtw_ctx *ctx, void *trace_dev)
+{
+    if (!ctx) return SDTW_EINVAL;
+    ctx->trace = static_cast<unsigned long long *>(trace_dev);
+    return SDTW_OK;
 }
 
 const char *sdtw_last_error(void) { return g_err.c_str(); }

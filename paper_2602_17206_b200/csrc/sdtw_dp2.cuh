@@ -41,21 +41,29 @@ __device__ __forceinline__ void load_group(T *dst, const T *src, int lane)
 }
 
 // Forward cell, interior case: softmin over (0, u, l) with 2 ex2 + 1 lg2.
+// min/max via fmin/fmax (one FMNMX each; inputs are finite or +/-inf, never
+// NaN), and v = (d - u) + sm, h = (d - l) + sm so the softmin is the last
+// addition on the dependency chain into the next step's shuffle.
+__device__ __forceinline__ float tmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ float tmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double tmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); }
+
 template <class T>
 __device__ __forceinline__ void fwd_cell(T d, T u, T l, T k, T gln2, T &g, T &v, T &h)
 {
-    const T lo = u < l ? u : l;
-    const T hi = u < l ? l : u;
-    const T mn = lo < T(0) ? lo : T(0);
-    const T mx = hi > T(0) ? hi : T(0);
-    const T hz = hi < T(0) ? hi : T(0);
-    const T md = lo > hz ? lo : hz;
+    const T lo = tmin(u, l);
+    const T hi = tmax(u, l);
+    const T mn = tmin(lo, T(0));
+    const T mx = tmax(hi, T(0));
+    const T md = tmax(lo, tmin(hi, T(0)));
     const T e1 = Num<T>::ex2((mn - md) * k);
     const T e2 = Num<T>::ex2((mn - mx) * k);
     const T s = (e1 + e2) + T(1);
-    g = d + (mn - gln2 * Num<T>::lg2(s));
-    v = g - u;
-    h = g - l;
+    const T sm = mn - gln2 * Num<T>::lg2(s);
+    g = d + sm;
+    v = (d - u) + sm;
+    h = (d - l) + sm;
 }
 
 template <class T, int K, bool kFused>

@@ -54,6 +54,20 @@ struct Tagged<float> {
     {
         return __uint_as_float((unsigned)(*p & 0xffffffffull));
     }
+    static __device__ __forceinline__ void store_if(Ent *p, float v, unsigned tag, bool pred)
+    {
+        const Ent w = ((Ent)tag << 32) | (Ent)__float_as_uint(v);
+        asm volatile(
+            "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.relaxed.gpu.global.b64 [%0], %1;\n\t}" ::"l"(p),
+            "l"(w), "r"((int)pred)
+            : "memory");
+    }
+    static __device__ __forceinline__ Ent load_raw(const Ent *p)
+    {
+        Ent w;
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+        return w;
+    }
 };
 
 template <>
@@ -79,6 +93,10 @@ struct Tagged<double> {
         return true;
     }
     static __device__ __forceinline__ double value(const Ent *p) { return p->v; }
+    static __device__ __forceinline__ void store_if(Ent *p, double v, unsigned tag, bool pred)
+    {
+        if (pred) store(p, v, tag);
+    }
 };
 
 template <class T>
@@ -99,7 +117,15 @@ struct Dp3Args {
     int4 *tile_meta;               // [cap] (b, s, c, width)
     unsigned tile_cap;
     unsigned *stats;               // [0] live tiles, [1] tiles stored, [2] overflow (in-warp)
+    unsigned long long *trace;     // optional [B*S][2] %globaltimer at strip start / end (forward)
 };
+
+__device__ __forceinline__ unsigned long long global_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Fixed-point exponents: |sum_j E_ij y_jk| <= M max|y| (E <= 1), etc.
 struct FxScales {
@@ -194,10 +220,26 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
             dsrc[q] = kFused ? nullptr : a.dsk + ((size_t)b * a.S + min(s0 + q, a.S - 1)) * (size_t)a.KK * 32;
         }
         const int qlast = min(K, a.S - s0) - 1;
-        double lacc = 0.0;
+        if (A.trace && t == 0) A.trace[2 * ((size_t)b * a.S + s0)] = global_ns();
+        double lacc = 0.0;  // tail terms (slow path only)
+        T gdiag[K];         // this lane's diagonal cell g (at most one per strip)
+        int kdiag[K];       // step at which lane t of strip q meets i == j
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            gdiag[q] = T(0);
+            kdiag[q] = 32 * s0 + 64 * q + 2 * t;
+        }
         const typename TG::Ent *hb_top = A.hbt + ((size_t)b * a.S + (s0 - 1)) * a.M;
         const int ngroups_row = a.KK / 32;
         const int steps = a.M + 32 * qlast + 31;
+        // A group is "plain" when every cell it touches is interior: no row 1,
+        // no column 1, no tail cell (row N with M > N, column M with N > M),
+        // and fully in band.  Plain and fill/drain groups share one
+        // branch-free step body; only boundary / tail / band fix-ups differ.
+        const bool has_row1 = s0 == 0;
+        const bool has_rowN = 32 * (s0 + qlast + 1) >= a.N;
+        unsigned long long pf_w = 0;  // prefetched halo entry (lanes 0..7)
+        int pf_kb = -1;
         if (!kFused) {
             load_group(ring, dsrc[0], t);
             cp_async_commit();
@@ -216,60 +258,145 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                 cp_async_wait<1>();
                 __syncwarp();
             }
+            // columns touched by this group (0-based): [k0 - 32 qlast - 31, k0 + 31]
+            const int cmin = k0 - 32 * qlast - 31, cmax = k0 + 31;
+            const bool fixup = has_row1 || cmin <= 0 ||
+                               (a.bw != 0 && (32 * s0 - k0 - 31 < -a.bw || 32 * s0 + 64 * qlast + 62 - k0 > a.bw));
+            const bool tail = (has_rowN && a.M > a.N && cmax >= a.N) || (a.N > a.M && cmax >= a.M - 1);
+            T vck[K];
+#pragma unroll
+            for (int q = 0; q < K; ++q) vck[q] = T(0);
 #pragma unroll 1
             for (int k8 = 0; k8 < 32; k8 += 8) {
                 const int kb = k0 + k8;
-                // top halo for columns [kb, kb + 8): polled as data (no flags)
+                // top halo for columns [kb, kb + 8): polled as data (no flags),
+                // the next sub-group prefetched
                 if (s0 > 0 && kb < a.M) {
                     const int n = min(8, a.M - kb);
-                    const T hv = poll_entries<T>(hb_top + kb, n, epoch, t);
+                    T hv = T(0);
+                    if constexpr (sizeof(T) == 4) {
+                        bool ok = t >= n;
+                        if (!ok) {
+                            unsigned long long w8 = (pf_kb == kb) ? pf_w : TG::load_raw(hb_top + kb + t);
+                            ok = (unsigned)(w8 >> 32) == epoch;
+                            hv = __uint_as_float((unsigned)(w8 & 0xffffffffull));
+                        }
+                        if (!__all_sync(kFull, ok)) hv = poll_entries<T>(hb_top + kb, n, epoch, t);
+                        const int kb2 = kb + 8;
+                        if (kb2 < a.M && t < min(8, a.M - kb2)) {
+                            pf_w = TG::load_raw(hb_top + kb2 + t);
+                            pf_kb = kb2;
+                        }
+                    } else {
+                        hv = poll_entries<T>(hb_top + kb, n, epoch, t);
+                    }
                     if (t < n) halo_s[(kb + t) & 31] = hv;
                     __syncwarp();
                 }
-#pragma unroll 2
-                for (int kk = 0; kk < 8; ++kk) {
-                    const int k = kb + kk;
-                    T src[K], u[K];
+                if (fixup || tail) {
 #pragma unroll
-                    for (int q = 0; q < K; ++q)
-                        src[q] = (t == 31) ? (q == 0 ? halo_s[k & 31] : h_prev[q - 1]) : h_prev[q];
-#pragma unroll
-                    for (int q = 0; q < K; ++q) u[q] = __shfl_sync(kFull, src[q], (t + 31) & 31);
-#pragma unroll
-                    for (int q = 0; q < K; ++q) {
-                        const int kq = k - 32 * q;
-                        const int col = kq - t;
-                        const int i = row[q], j = col + 1;
-                        if (!(row_ok[q] && col >= 0 && col < a.M)) continue;
-                        T d;
-                        if (kFused) {
-                            d = load_cost<T, true>(a, b, s0 + q, t, i, j);
-                        } else {
-                            d = ring[(q * 2 + ((kq >> 5) & 1)) * 1024 + (kq & 31) * 32 + t];
-                        }
-                        T g, v, h;
-                        if (i > 1 && j > 1 && in_band(i, j, a.bw)) {
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int k = kb + kk;
+                        const int kl = k8 + kk;  // step within the group
+                        T src[K], u[K];
+                        const T hs = halo_s[kl];
+    #pragma unroll
+                        for (int q = 0; q < K; ++q) src[q] = (t == 31) ? (q == 0 ? hs : h_prev[q - 1]) : h_prev[q];
+    #pragma unroll
+                        for (int q = 0; q < K; ++q) u[q] = __shfl_sync(kFull, src[q], (t + 31) & 31);
+    #pragma unroll
+                        for (int q = 0; q < K; ++q) {
+                            const int col = k - 32 * q - t;  // 0-based column of this lane's cell
+                            const bool active = row_ok[q] && col >= 0 && col < a.M;
+                            T d;
+                            if (kFused) {
+                                d = active ? load_cost<T, true>(a, b, s0 + q, t, row[q], col + 1) : T(0);
+                            } else {
+                                d = ring[(q * 2 + ((G - q) & 1)) * 1024 + kl * 32 + t];
+                            }
+                            T g, v, h;
                             fwd_cell<T>(d, u[q], l_carry[q], a.k, a.gln2, g, v, h);
-                        } else if (!in_band(i, j, a.bw)) {
-                            g = inf; v = inf; h = inf;
-                        } else if (i == 1 && j == 1) {
-                            g = d; v = -inf; h = -inf;
-                        } else if (i == 1) {
-                            g = d; h = d; v = -inf;
-                        } else {
-                            g = d; v = d; h = -inf;
+                            if (fixup) {  // warp-uniform: boundary row / column, band
+                                const bool j1 = col == 0, r1 = row[q] == 1;
+                                g = (j1 || r1) ? d : g;
+                                v = r1 ? -inf : (j1 ? d : v);
+                                h = j1 ? -inf : (r1 ? d : h);
+                                if (a.bw != 0 && !in_band(row[q], col + 1, a.bw)) {
+                                    g = inf; v = inf; h = inf;
+                                }
+                            }
+                            if (tail && active) {  // warp-uniform branch, rare
+                                const int i = row[q], j = col + 1;
+                                if (i == a.N && j > a.N) lacc += (double)h;
+                                if (j == a.M && i > a.M) lacc += (double)v;
+                            }
+                            gdiag[q] = (active && k == kdiag[q]) ? g : gdiag[q];
+                            vck[q] = (kl == ((t - 1) & 31)) ? v : vck[q];
+                            l_carry[q] = v;
+                            h_prev[q] = h;
+                            // lane 31: bottom row of the strip (predicated, no divergence)
+                            TG::store_if(A.hbt + ((size_t)b * a.S + (s0 + q)) * a.M + col, h, epoch, t == 31 && active);
                         }
-                        if (i == j) lacc += (double)g;
-                        if (i == a.N && j > a.N) lacc += (double)h;
-                        if (j == a.M && i > a.M) lacc += (double)v;
-                        if ((j & 31) == 0 && j < a.M) a.vc[((size_t)b * a.C + (j / 32 - 1)) * a.N + (i - 1)] = v;
-                        l_carry[q] = v;
-                        h_prev[q] = h;
-                        if (t == 31) TG::store(A.hbt + ((size_t)b * a.S + (s0 + q)) * a.M + col, h, epoch);
+                    }
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int k = kb + kk;
+                        const int kl = k8 + kk;  // step within the group
+                        T src[K], u[K];
+                        const T hs = halo_s[kl];
+    #pragma unroll
+                        for (int q = 0; q < K; ++q) src[q] = (t == 31) ? (q == 0 ? hs : h_prev[q - 1]) : h_prev[q];
+    #pragma unroll
+                        for (int q = 0; q < K; ++q) u[q] = __shfl_sync(kFull, src[q], (t + 31) & 31);
+    #pragma unroll
+                        for (int q = 0; q < K; ++q) {
+                            const int col = k - 32 * q - t;  // 0-based column of this lane's cell
+                            const bool active = row_ok[q] && col >= 0 && col < a.M;
+                            T d;
+                            if (kFused) {
+                                d = active ? load_cost<T, true>(a, b, s0 + q, t, row[q], col + 1) : T(0);
+                            } else {
+                                d = ring[(q * 2 + ((G - q) & 1)) * 1024 + kl * 32 + t];
+                            }
+                            T g, v, h;
+                            fwd_cell<T>(d, u[q], l_carry[q], a.k, a.gln2, g, v, h);
+                            if (false) {
+                                const bool j1 = col == 0, r1 = row[q] == 1;
+                                g = (j1 || r1) ? d : g;
+                                v = r1 ? -inf : (j1 ? d : v);
+                                h = j1 ? -inf : (r1 ? d : h);
+                                if (a.bw != 0 && !in_band(row[q], col + 1, a.bw)) {
+                                    g = inf; v = inf; h = inf;
+                                }
+                            }
+                            if (false) {
+                                const int i = row[q], j = col + 1;
+                                if (i == a.N && j > a.N) lacc += (double)h;
+                                if (j == a.M && i > a.M) lacc += (double)v;
+                            }
+                            gdiag[q] = (active && k == kdiag[q]) ? g : gdiag[q];
+                            vck[q] = (kl == ((t - 1) & 31)) ? v : vck[q];
+                            l_carry[q] = v;
+                            h_prev[q] = h;
+                            // lane 31: bottom row of the strip (predicated, no divergence)
+                            TG::store_if(A.hbt + ((size_t)b * a.S + (s0 + q)) * a.M + col, h, epoch, t == 31 && active);
+                        }
                     }
                 }
             }
+            // chunk-boundary v captured in registers: lanes 1..31 hold column
+            // 32 (G - q) (1-based), lane 0 the next boundary
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                const int bidx = (t == 0) ? (G - q) : (G - q - 1);
+                const int jb = 32 * (bidx + 1);
+                if (bidx >= 0 && jb < a.M && row_ok[q]) a.vc[((size_t)b * a.C + bidx) * a.N + (row[q] - 1)] = vck[q];
+            }
         }
+#pragma unroll
+        for (int q = 0; q < K; ++q) lacc += (double)gdiag[q];
+        if (A.trace && t == 0) A.trace[2 * ((size_t)b * a.S + s0) + 1] = global_ns();
         if (!kFused) cp_async_wait<0>();
         for (int off = 16; off > 0; off >>= 1) lacc += __shfl_xor_sync(kFull, lacc, off);
         if (t == 0) {
