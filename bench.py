@@ -392,7 +392,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--mode", default="fused", choices=["fused", "unfused"])
+    ap.add_argument("--mode", default="unfused", choices=["fused", "unfused"])
     ap.add_argument("--single-mode", action="store_true", help="skip the other cost mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
