@@ -27,6 +27,7 @@
 #include "sdtw_dp.cuh"
 #include "sdtw_dp2.cuh"
 #include "sdtw_dp3.cuh"
+#include "sdtw_dp4.cuh"
 #include "sdtw_tc.cuh"
 
 namespace {
@@ -450,6 +451,7 @@ struct Pipeline {
 
     using Ent = typename sdtw::Tagged<T>::Ent;
     Ent *hbt = nullptr, *sbt = nullptr;
+    unsigned long long *stat = nullptr;
     unsigned epoch = 0;
     Buf<long long> gx_fx, gy_fx, rs_fx, cs_fx;
     Buf<T> tiles;
@@ -459,7 +461,7 @@ struct Pipeline {
 
     void halos()
     {
-        const size_t need = 2 * (size_t)B * S * M * sizeof(Ent);
+        const size_t need = 2 * (size_t)B * S * M * sizeof(Ent) + (size_t)B * S * C * 8;
         if (ctx->halo_bytes < need) {
             if (ctx->halo_arena) {
                 CUDA_OK(cudaStreamSynchronize(ctx->stream));
@@ -477,6 +479,7 @@ struct Pipeline {
         }
         hbt = static_cast<Ent *>(ctx->halo_arena);
         sbt = hbt + (size_t)B * S * M;
+        stat = reinterpret_cast<unsigned long long *>(sbt + (size_t)B * S * M);
         epoch = ++ctx->epoch;
         if (epoch == 0) epoch = ++ctx->epoch;
     }
@@ -569,16 +572,14 @@ struct Pipeline {
         auto A = args3();
         {
             Phase ph(ctx, 3);
-            const int threads = sizeof(T) == 4 ? 128 : 64;
-            const int wpc = threads / 32;
             if (fused) {
-                auto kern = sdtw::sdtw_backward3_kernel<T, true>;
-                const size_t smem = wpc * sdtw::Bwd3Smem<T, true>::kPerWarp * sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * S), threads, smem, A);
+                auto kern = sdtw::sdtw_backward4_kernel<T, true>;
+                const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);
+                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat);
             } else {
-                auto kern = sdtw::sdtw_backward3_kernel<T, false>;
-                const size_t smem = wpc * sdtw::Bwd3Smem<T, false>::kPerWarp * sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * S), threads, smem, A);
+                auto kern = sdtw::sdtw_backward4_kernel<T, false>;
+                const size_t smem = sdtw::Bwd4Smem<T, false>::kPerWarp * sizeof(T);
+                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat);
             }
         }
         {

@@ -420,15 +420,15 @@ using Bwd3Smem = Bwd2Smem<T, kFused>;
 // (32 rows x 32 features per round, 4 KB of T).
 template <class T>
 __device__ __forceinline__ void tile_contract_fx(const Dp3Args<T> &A, const FxScales &fx, int b, int s, int c,
-                                                 int width, const T *et_s, T *stage, int t)
+                                                 int width, const T *et_s, T *stage, int t, int es = 32)
 {
     const DpArgs<T> &a = A.a;
     const int i0 = 32 * s, j0 = 32 * c;  // 0-based
     const int D = a.D;
     const int rows = min(32, a.N - i0);
     T rs = T(0), cs = T(0);
-    for (int jj = 0; jj < width; ++jj) rs += et_s[t * 32 + jj];
-    for (int r = 0; r < rows; ++r) cs += et_s[r * 32 + t];
+    for (int jj = 0; jj < width; ++jj) rs += et_s[t * es + jj];
+    for (int r = 0; r < rows; ++r) cs += et_s[r * es + t];
     if (t < rows) fx_add(A.rs_fx + (size_t)b * a.N + i0 + t, (double)rs, fx.rs);
     if (t < width) fx_add(A.cs_fx + (size_t)b * a.M + j0 + t, (double)cs, fx.cs);
     for (int pass = 0; pass < 2; ++pass) {
@@ -447,7 +447,7 @@ __device__ __forceinline__ void tile_contract_fx(const Dp3Args<T> &A, const FxSc
 #pragma unroll
             for (int q = 0; q < 32; ++q) acc[q] = T(0);
             for (int m = 0; m < nsrc; ++m) {
-                const T e = pass == 0 ? et_s[t * 32 + m] : et_s[m * 32 + t];
+                const T e = pass == 0 ? et_s[t * es + m] : et_s[m * es + t];
 #pragma unroll
                 for (int q = 0; q < 32; ++q) acc[q] = fma(e, stage[m * 33 + q], acc[q]);
             }
