@@ -76,10 +76,12 @@ _lib = None
 
 
 def load_library(path: str = LIB_PATH) -> C.CDLL:
-    """Loads libsdtw_b200.so; raises ImportError if it was not built."""
+    """Loads libsdtw_b200.so; raises ImportError if it was not built.
+    SDTW_LIB overrides the path (experiment builds)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("SDTW_LIB", path)
     if not os.path.exists(path):
         raise ImportError(
             f"CUDA engine library missing at {path}: run `python -m paper_2602_17206_b200.build` "

@@ -28,6 +28,7 @@
 #include "sdtw_dp2.cuh"
 #include "sdtw_dp3.cuh"
 #include "sdtw_dp4.cuh"
+#include "sdtw_fused.cuh"
 #include "sdtw_tc.cuh"
 
 namespace {
@@ -352,6 +353,19 @@ struct Pipeline {
         S = (N + 31) / 32;
         C = (M + 31) / 32;
         KK = ((M + 62) / 32) * 32;
+        dpad = ((D + 63) / 64) * 64;
+        tc_fused = fused && std::is_same<T, float>::value && dpad <= sdtw::kFtcMaxD;
+    }
+
+    // fp32 fused mode with D <= 128 runs on the tensor cores (sdtw_fused.cuh);
+    // fp64 (and D > 128) fused mode computes each cost with a SIMT dot.
+    int dpad = 64;
+    bool tc_fused = false;
+    sdtw::FusedTcArgs ftc() const
+    {
+        sdtw::FusedTcArgs f{};
+        f.dpad = dpad;
+        return f;
     }
 
     sdtw::DpArgs<T> args()
@@ -399,7 +413,7 @@ struct Pipeline {
 
     void costs()
     {
-        if (fused) return;
+        if (fused) return;  // costs are computed inside the DP kernels
         Phase ph(ctx, 1);
         const size_t total = (size_t)B * S * KK * 32;
         dsk = Buf<T>(ctx, total);
@@ -534,7 +548,21 @@ struct Pipeline {
         // strips per warp: enough warps to fill the device first, ILP second
         const int strips = B * S;
         const int slots = ctx->sm_count * 16;
-        if (strips >= 4 * slots) launch_forward3<4>();
+        if (tc_fused) {
+            if constexpr (std::is_same<T, float>::value) {
+                auto A = args3();
+                const size_t smem = 2 * sdtw::ftc_slot_bytes(dpad);
+                static size_t attr = 0;
+                if (attr != smem) {
+                    CUDA_OK(cudaFuncSetAttribute(sdtw::sdtw_forward_tc_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    attr = smem;
+                }
+                const int work = B * ((S + 3) / 4);
+                const unsigned grid = (unsigned)std::max(1, std::min((work + 1) / 2, ctx->sm_count));
+                LAUNCH(ctx, sdtw::sdtw_forward_tc_kernel, grid, sdtw::kFtcThreads, smem, A, ftc());
+            }
+        } else if (strips >= 4 * slots) launch_forward3<4>();
         else if (strips >= 2 * slots) launch_forward3<2>();
         else launch_forward3<1>();
         LAUNCH(ctx, sdtw::sdtw_loss_reduce_kernel, grid_for(B, 128), 128, 0, lpart.p, B, S, loss_f,
@@ -572,14 +600,22 @@ struct Pipeline {
         auto A = args3();
         {
             Phase ph(ctx, 3);
-            if (fused) {
+            if (tc_fused) {
+                auto kern = sdtw::sdtw_backward4_kernel<T, false, true>;
+                const size_t smem = sdtw::Bwd4Smem<T, false, true>::kPerWarp * sizeof(T);
+                // every CTA holds 128 TMEM columns for its lifetime: at most
+                // 4 may be resident on an SM (the shared memory guarantees it)
+                static_assert(sdtw::Bwd4Smem<float, false, true>::kPerWarp * 4 > 233472 / 5,
+                              "fused backward CTA must not fit 5 per SM");
+                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat, ftc());
+            } else if (fused) {
                 auto kern = sdtw::sdtw_backward4_kernel<T, true>;
                 const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat);
+                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat, sdtw::FusedTcArgs{});
             } else {
                 auto kern = sdtw::sdtw_backward4_kernel<T, false>;
                 const size_t smem = sdtw::Bwd4Smem<T, false>::kPerWarp * sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat);
+                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat, sdtw::FusedTcArgs{});
             }
         }
         {

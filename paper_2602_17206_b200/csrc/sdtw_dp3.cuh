@@ -41,12 +41,12 @@ struct Tagged<float> {
     static __device__ __forceinline__ void store(Ent *p, float v, unsigned tag)
     {
         const Ent w = ((Ent)tag << 32) | (Ent)__float_as_uint(v);
-        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+        asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w));
     }
     static __device__ __forceinline__ bool load(const Ent *p, float &v, unsigned tag)
     {
         Ent w;
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p));
         v = __uint_as_float((unsigned)(w & 0xffffffffull));
         return (unsigned)(w >> 32) == tag;
     }
@@ -60,12 +60,12 @@ struct Tagged<float> {
         asm volatile(
             "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.relaxed.gpu.global.b64 [%0], %1;\n\t}" ::"l"(p),
             "l"(w), "r"((int)pred)
-            : "memory");
+           );
     }
     static __device__ __forceinline__ Ent load_raw(const Ent *p)
     {
         Ent w;
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p));
         return w;
     }
 };
@@ -236,7 +236,9 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
         // no column 1, no tail cell (row N with M > N, column M with N > M),
         // and fully in band.  Plain and fill/drain groups share one
         // branch-free step body; only boundary / tail / band fix-ups differ.
-        const bool has_row1 = s0 == 0;
+        // lane 0 of a pair's first strip is row 1 (R(0, j) = inf): three
+        // selects in every step instead of the fix-up path for the whole strip
+        const bool r1 = s0 == 0 && t == 0;
         const bool has_rowN = 32 * (s0 + qlast + 1) >= a.N;
         unsigned long long pf_w = 0;  // prefetched halo entry (lanes 0..7)
         int pf_kb = -1;
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
             }
             // columns touched by this group (0-based): [k0 - 32 qlast - 31, k0 + 31]
             const int cmin = k0 - 32 * qlast - 31, cmax = k0 + 31;
-            const bool fixup = has_row1 || cmin <= 0 ||
+            const bool fixup = cmin <= 0 ||
                                (a.bw != 0 && (32 * s0 - k0 - 31 < -a.bw || 32 * s0 + 64 * qlast + 62 - k0 > a.bw));
             const bool tail = (has_rowN && a.M > a.N && cmax >= a.N) || (a.N > a.M && cmax >= a.M - 1);
             T vck[K];
@@ -316,6 +318,11 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                             }
                             T g, v, h;
                             fwd_cell<T>(d, u[q], l_carry[q], a.k, a.gln2, g, v, h);
+                            if (q == 0) {
+                                g = r1 ? d : g;
+                                v = r1 ? -inf : v;
+                                h = r1 ? d : h;
+                            }
                             if (fixup) {  // warp-uniform: boundary row / column, band
                                 const bool j1 = col == 0, r1 = row[q] == 1;
                                 g = (j1 || r1) ? d : g;
@@ -361,6 +368,11 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                             }
                             T g, v, h;
                             fwd_cell<T>(d, u[q], l_carry[q], a.k, a.gln2, g, v, h);
+                            if (q == 0) {
+                                g = r1 ? d : g;
+                                v = r1 ? -inf : v;
+                                h = r1 ? d : h;
+                            }
                             if (false) {
                                 const bool j1 = col == 0, r1 = row[q] == 1;
                                 g = (j1 || r1) ? d : g;

@@ -17,9 +17,11 @@
 //   * runs of dead tiles are skipped 32 chunks per status load.
 // Tile skipping, checkpoints and the gradient hand-off are those of v3.
 #pragma once
+#include <type_traits>
 #include "sdtw_common.cuh"
 #include "sdtw_dp2.cuh"
 #include "sdtw_dp3.cuh"
+#include "sdtw_fused.cuh"
 
 namespace sdtw {
 
@@ -34,26 +36,31 @@ namespace sdtw {
 enum : unsigned { kTileDead = 1u, kTileHint = 2u, kTileLive = 3u, kTileCommit = 4u };
 constexpr unsigned kSpecDepth = 2;
 
-template <class T, bool kFused>
+template <class T, bool kFused, bool kTc = false>
 struct Bwd4Smem {
+    // kTc: the strip's x rows as a packed fp16 hi/lo tensor-core operand
+    // (32 rows x kFtcMaxD), placed first so that the unused rows 32..127 of
+    // the M = 128 MMA read (harmlessly) into the probability slots after it
+    static constexpr int kX = kTc ? kFtcMaxD * 32 * 4 / (int)sizeof(T) : 0;
     static constexpr int kSlot = 3 * 33 * 32;            // pd, pu, pl [jj][t], row 32 = dummy
     static constexpr int kP = 3 * kSlot;                 // three probability tiles
     static constexpr int kE = 32 * 34;                   // E tile [t][jj] (even stride: conflict-free), column 32 = dummy
-    static constexpr int kRing = kFused ? 0 : 4 * 1024;  // skewed cost row groups (slot g & 3)
+    static constexpr int kRing = (kFused && !kTc) ? 0 : 4 * 1024;  // skewed cost row groups (slot g & 3)
     static constexpr int kHalo = 6 * 32;                 // 3 top halos (h), S in, S out (+dummy)
-    static constexpr int kPerWarp = kP + kE + kRing + kHalo;
+    static constexpr int kBar = kTc ? 16 / (int)sizeof(T) + 2 : 0;  // 2 mbarriers + TMEM base (kTc)
+    static constexpr int kPerWarp = kX + kP + kE + kRing + kHalo + kBar;
 };
 
 // Status words: (epoch << 32) | status.
 __device__ __forceinline__ void put_status(unsigned long long *p, unsigned v, unsigned tag)
 {
     const unsigned long long w = ((unsigned long long)tag << 32) | v;
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w));
 }
 __device__ __forceinline__ unsigned get_status(const unsigned long long *p, unsigned tag)
 {
     unsigned long long w;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p));
     return (unsigned)(w >> 32) == tag ? (unsigned)(w & 0xffffffffull) : 0u;
 }
 
@@ -85,15 +92,41 @@ __device__ __forceinline__ T bwd_cost(const DpArgs<T> &a, const T *ring, int b, 
     return ring[((kk >> 5) & 3) * 1024 + (kk & 31) * 32 + t];
 }
 
-template <class T, bool kFused>
-__global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsigned long long *stat)
+// kTc (fp32 fused mode): the cost blocks of the recomputed tiles come from
+// tcgen05.mma (sdtw_fused.cuh) into TMEM, through the same epilogue and into
+// the same skewed ring the unfused path fills from the cost tensor.  The warp
+// is warp 0 of its CTA, so it owns TMEM lanes 0..31: its strip's 32 rows are
+// rows 0..31 of an M = 128 MMA whose other rows are don't-care.
+template <class T, bool kFused, bool kTc = false>
+__global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsigned long long *stat,
+                                                            FusedTcArgs F)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const DpArgs<T> &a = A.a;
-    using SM = Bwd4Smem<T, kFused>;
+    using SM = Bwd4Smem<T, kFused, kTc>;
     using TG = Tagged<T>;
     const int t = threadIdx.x & 31;
-    T *base = reinterpret_cast<T *>(smem_raw);
+    uint8_t *xs = smem_raw;  // kTc: packed x rows of the strip
+    T *base = reinterpret_cast<T *>(smem_raw) + SM::kX;
+    // kTc: [0] MMA done, [1] operand copies landed; then the TMEM base
+    uint64_t *tc_bar = reinterpret_cast<uint64_t *>(base + SM::kP + SM::kE + SM::kRing + SM::kHalo);
+    uint32_t &tc_tmem = *reinterpret_cast<uint32_t *>(tc_bar + 2);
+    uint32_t tc_ph[2] = {0u, 0u};
+    uint32_t tmem = 0;
+    float tc_m2 = 0.f;
+    if constexpr (kTc) {
+        if (t == 0) {
+            tc::mbar_init(&tc_bar[0], 1);
+            tc::mbar_init(&tc_bar[1], 1);
+            tc::fence_barrier_init();
+        }
+        tc::tmem_alloc<128>(&tc_tmem);
+        tc::tc_fence_before();
+        __syncwarp();
+        tc::tc_fence_after();
+        tmem = tc_tmem;
+        tc_m2 = -2.0f * split_scale(A.absmax).inv;
+    }
     // probability tile slots k = 0..2 at base + kSlot k: pd, pu, pl [jj][t]
     constexpr int kSlot = SM::kSlot;
     T *et_s = base + SM::kP;
@@ -107,10 +140,12 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
     const FxScales fx = fx_scales(A.absmax, a.N, a.M);
     for (;;) {
         const unsigned tk = warp_ticket(&a.tickets[1]);
-        if ((int)tk >= total) return;
+        if ((int)tk >= total) break;
         const int s = a.S - 1 - (int)tk / a.B, b = (int)tk % a.B;
         const int i = 32 * s + t + 1;
         const bool row_ok = i <= a.N;
+        bool x_loaded = false;
+        const float tc_xi = (kTc && row_ok) ? (float)a.xn[(size_t)b * a.N + i - 1] : 0.f;
         const bool bottom = s == a.S - 1;
         const T *dsrc = kFused ? nullptr : a.dsk + ((size_t)b * a.S + s) * (size_t)a.KK * 32;
         unsigned long long *stat_me = stat + ((size_t)b * a.S + s) * a.C;
@@ -119,6 +154,17 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
         const typename TG::Ent *sb_below = A.sbt + ((size_t)b * a.S + s + 1) * a.M;
         if (A.trace && t == 0) A.trace[2 * ((size_t)a.B * a.S + (size_t)b * a.S + s)] = global_ns();
         int ntiles = 0;
+        // cycle accounting (trace mode): [32 B S + 8 (b S + s) + e]: e = 0
+        // recompute, 1 S wait, 2 E steps, 3 status waits, 4 tile epilogue, 5 other
+        long long cyc[6] = {0, 0, 0, 0, 0, 0};
+        long long c_mark = A.trace ? clock64() : 0;
+        auto lap = [&](int e) {
+            if (A.trace) {
+                const long long now = clock64();
+                cyc[e] += now - c_mark;
+                c_mark = now;
+            }
+        };
         auto ev = [&](int e) {
             if (A.trace && t == 0 && e < 8)
                 A.trace[5 * (size_t)a.B * a.S + 8 * ((size_t)b * a.S + s) + e] = global_ns();
@@ -127,12 +173,77 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
         // P-tile cache: slot k holds chunk slot_c[k] (-1: none)
         int slot_c0 = -1, slot_c1 = -1, slot_c2 = -1;
         auto find_slot = [&](int cf) { return slot_c0 == cf ? 0 : slot_c1 == cf ? 1 : slot_c2 == cf ? 2 : -1; };
+        // kTc: cost blocks of chunks cr, cr-1, .. (nt of them) -> skewed ring.
+        // Operands: the strip's x rows (loaded once per strip) and the y
+        // chunks, staged K-half by K-half in the probability slots (free
+        // until the recompute loop writes them).
+        auto tc_costs = [&](int cr, int nt, bool &xl, int b_, int s_, int i_, bool rok, float xi) {
+            if constexpr (kTc) {
+                const int dpad = F.dpad;
+                uint8_t *stage = reinterpret_cast<uint8_t *>(base);
+                const uint32_t idesc = tc::idesc_f16_f32(128, 32);
+                const SplitScale sc = split_scale(A.absmax);
+                if (!xl) {
+                    stage_split_rows(reinterpret_cast<const float *>(a.x) + (size_t)b_ * a.N * a.D, a.D, 32 * s_, 32, a.N,
+                                     a.D, dpad, sc.sx, xs, t);
+                    xl = true;
+                }
+                for (int kh = 0; kh < dpad / 64; ++kh) {
+                    // y chunks cr - z, features [64 kh, 64 kh + 64): 32 rows x 64
+                    for (int z = 0; z < nt; ++z)
+                        stage_split_rows(reinterpret_cast<const float *>(a.y) + (size_t)b_ * a.M * a.D +
+                                             (size_t)64 * kh,
+                                         a.D, 32 * (cr - z), 32, a.M, a.D - 64 * kh, 64, sc.sy, stage + z * 8192, t);
+                    tc::fence_async_smem();
+                    __syncwarp();
+                    tc::tc_fence_after();
+                    if (t == 0) {
+                        const uint32_t xh = tc::smem_u32(xs), xlo = xh + 32u * dpad * 2;
+                        for (int z = 0; z < nt; ++z) {
+                            const uint32_t bh = tc::smem_u32(stage + z * 8192), bl = bh + 4096;
+                            for (int ks = 0; ks < 4; ++ks) {
+                                const int kg = 4 * kh + ks;
+                                const uint32_t oa = kg * 1024, ob = ks * 1024;
+                                const uint32_t acc0 = kg > 0 ? 1u : 0u;
+                                const uint32_t d = tmem + 32u * z;
+                                tc::mma_f16(d, tc::smem_desc(xh + oa, 512, 128), tc::smem_desc(bh + ob, 512, 128), idesc, acc0);
+                                tc::mma_f16(d, tc::smem_desc(xh + oa, 512, 128), tc::smem_desc(bl + ob, 512, 128), idesc, 1u);
+                                tc::mma_f16(d, tc::smem_desc(xlo + oa, 512, 128), tc::smem_desc(bh + ob, 512, 128), idesc, 1u);
+                            }
+                        }
+                        tc::mma_commit(&tc_bar[0]);
+                    }
+                    __syncwarp();
+                    tc::mbar_wait(&tc_bar[0], tc_ph[0]);
+                    tc_ph[0] ^= 1u;
+                    tc::tc_fence_after();
+                }
+                for (int z = 0; z < nt; ++z) {
+                    float acc[32];
+                    tc::tmem_ld32(tmem + 32u * z, acc);
+                    const int j0 = 32 * (cr - z);
+                    const float yv = (j0 + t < a.M) ? (float)a.yn[(size_t)b_ * a.M + j0 + t] : 0.f;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float yj = __shfl_sync(kFull, yv, e);
+                        const int j = j0 + e;
+                        const bool ok = rok && j < a.M && in_band(i_, j + 1, a.bw);
+                        const int kk = j + t;
+                        ring[((kk >> 5) & 3) * 1024 + (kk & 31) * 32 + t] = (T)tc_cost(acc[e], xi, yj, tc_m2, ok);
+                    }
+                }
+                tc::tc_fence_before();
+            }
+        };
         // recompute tile cr and, speculatively, cr-1 and cr-2 (independent
         // tiles in one skewed loop: ILP 3); tile cr - z lands in slot z
         auto recompute = [&](int cr) {
+            lap(5);
             const int wr = min(32, a.M - 32 * cr);
             const int nt = min(3, cr + 1);
-            if (!kFused) {
+            if constexpr (kTc) {
+                tc_costs(cr, nt, x_loaded, b, s, i, row_ok, tc_xi);
+            } else if (!kFused) {
                 for (int g = cr - 2; g <= cr + 1; ++g)
                     if (g >= 0 && g < ngroups_row) load_group(ring + (g & 3) * 1024, dsrc + (size_t)g * 1024, t);
                 cp_async_commit();
@@ -148,7 +259,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                                          ? TG::value(A.hbt + ((size_t)b * a.S + (s - 1)) * a.M + 32 * cz + t)
                                          : T(0);
             }
-            if (!kFused) cp_async_wait<0>();
+            if (!kFused && !kTc) cp_async_wait<0>();
             __syncwarp();
             // tiles touching row 1, column 1 or a band edge take the general
             // cell; all others a branch-free one (warp-uniform choice)
@@ -184,6 +295,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                 }
             }
             __syncwarp();
+            lap(0);
             slot_c0 = cr;
             slot_c1 = nt > 1 ? cr - 1 : -1;
             slot_c2 = nt > 2 ? cr - 2 : -1;
@@ -212,6 +324,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                 unsigned st = kTileHint;  // lanes past chunk 0 never stop a dead run
                 if (cc >= 0) st = get_status(stat_below + cc, epoch);
                 unsigned polls = 0;
+                lap(5);
                 while (!__shfl_sync(kFull, st, 0)) {  // chunk c's status must be known
                     __nanosleep(32);
                     if (cc >= 0 && st == 0) st = get_status(stat_below + cc, epoch);
@@ -220,6 +333,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                         break;
                     }
                 }
+                lap(3);
                 const unsigned stop = __ballot_sync(kFull, st != kTileDead);
                 const int run = stop ? __ffs(stop) - 1 : 32;  // leading dead chunks
                 if (run > 0) {
@@ -237,6 +351,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                     if (find_slot(c) < 0) recompute(c);
                     if (st0 + 1 < kTileCommit + kSpecDepth && t == 0) put_status(stat_me + c, st0 + 1, epoch);
                     polls = 0;
+                    lap(5);
                     while (st0 >= kTileCommit) {
                         __nanosleep(64);
                         st0 = __shfl_sync(kFull, get_status(stat_below + c, epoch), 0);
@@ -245,6 +360,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                             break;
                         }
                     }
+                    lap(3);
                     if (st0 == kTileDead) {
                         dead_chunk(c);
                         pl_right = T(0);
@@ -272,9 +388,26 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
             T s_prev = T(0);
             unsigned long long pf_w = 0;
             int pf_q = -1;
-            for (int q = 0; q < width + 31; ++q) {
-                const int jj31 = width - 1 - q;
-                if (((q & 7) == 0) && jj31 >= 0) {
+            lap(5);
+            // 8-step sub-groups: S from below polled once per sub-group, the
+            // sub-group's probabilities loaded up front (no shared load on the
+            // step chain), branch-free steps; S published as soon as lane 0
+            // completes a group of 8 columns (after step 6 of a sub-group).
+            int pub_next = 0;  // next 8-column group (from the right) to publish
+            auto publish = [&](int done) {
+                // groups k with all columns done (or the tile's last partial group)
+                while (8 * pub_next <= done && (8 * pub_next + 7 <= done || done >= width - 1)) {
+                    __syncwarp();
+                    const int hi = width - 1 - 8 * pub_next;
+                    const int lo = max(0, hi - 7);
+                    if (t <= hi - lo) TG::store(sb_me + (j0 - 1) + lo + t, sout_s[lo + t], epoch);
+                    ++pub_next;
+                }
+            };
+            for (int q8 = 0; q8 < width + 31; q8 += 8) {
+                const int jj31 = width - 1 - q8;
+                if (jj31 >= 0) {
+                    lap(2);
                     // S from below for columns [jj31 - 7, jj31] of this chunk
                     const int lo = max(0, jj31 - 7);
                     const int n = jj31 - lo + 1;
@@ -283,7 +416,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                         if constexpr (sizeof(T) == 4) {
                             bool ok = t >= n;
                             if (!ok) {
-                                const unsigned long long w8 = (pf_q == q) ? pf_w : TG::load_raw(sb_below + (j0 - 1) + lo + t);
+                                const unsigned long long w8 = (pf_q == q8) ? pf_w : TG::load_raw(sb_below + (j0 - 1) + lo + t);
                                 ok = (unsigned)(w8 >> 32) == epoch;
                                 v = __uint_as_float((unsigned)(w8 & 0xffffffffull));
                             }
@@ -293,12 +426,13 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                             if (jn >= 0) {
                                 const int lo2 = max(0, jn - 7);
                                 if (t <= jn - lo2) pf_w = TG::load_raw(sb_below + (j0 - 1) + lo2 + t);
-                                pf_q = q + 8;
+                                pf_q = q8 + 8;
                             }
                         } else {
                             v = poll_entries<T>(sb_below + (j0 - 1) + lo, n, epoch, t);
                         }
                     }
+                    lap(1);
                     if (t < n) sin_s[lo + t] = v;
                     if (!hinted && __any_sync(kFull, v != T(0))) {
                         hinted = true;
@@ -306,40 +440,56 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                     }
                     __syncwarp();
                 }
-                const int jj = width - 1 - q + (31 - t);
-                const T src = (t == 0) ? sin_s[jj31 >= 0 ? jj31 : 0] : s_prev;
-                const T s_in = __shfl_sync(kFull, src, (t + 1) & 31);
-                // branch-free step: inactive lanes read / write the dummy row
-                const bool act = jj >= 0 && jj < width;
-                const bool cell = act && row_ok;
-                const int jc = act ? jj : 32;
-                const T pd = Pc[jc * 32 + t], pu = Pc[1056 + jc * 32 + t], pl = Pc[2112 + jc * 32 + t];
-                const int j = j0 + jj;
-                T e = fma(e_right, pl_right, s_in);
-                e = e < T(1) ? e : T(1);
-                if (has_end_tile || a.bw != 0) {  // warp-uniform
-                    e = (i == a.N && j == a.M) ? T(1) : e;
-                    e = in_band(i, j, a.bw) ? e : T(0);
+                T pd8[8], pu8[8], pl8[8], si8[8];
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int q = q8 + kk;
+                    const int jj = width - 1 - q + (31 - t);
+                    const int jc = (jj >= 0 && jj < width) ? jj : 32;
+                    pd8[kk] = Pc[jc * 32 + t];
+                    pu8[kk] = Pc[1056 + jc * 32 + t];
+                    pl8[kk] = Pc[2112 + jc * 32 + t];
+                    const int j31 = width - 1 - q;
+                    si8[kk] = sin_s[j31 >= 0 ? j31 : 0];
                 }
-                e = cell ? e : T(0);
-                const T s_out = cell ? fma(e, pu, e_right * pd_right) : s_prev;
-                e_right = cell ? e : e_right;
-                pl_right = cell ? pl : pl_right;
-                pd_right = cell ? pd : pd_right;
-                et_s[t * 34 + jc] = e;
-                if (t == 0) sout_s[jc] = s_out;
-                s_prev = s_out;
-                // lane 0 finished column jj0 = width-1-(q-31): publish each
-                // completed group of 8 columns
-                const int done = q - 31;  // columns completed by lane 0 minus 1
-                if (done >= 0 && (((done & 7) == 7) || done == width - 1)) {
-                    __syncwarp();
-                    const int hi = width - 1 - (done & ~7);
-                    const int lo = width - 1 - done;
-                    if (t <= hi - lo) TG::store(sb_me + (j0 - 1) + lo + t, sout_s[lo + t], epoch);
-                }
+                auto esteps = [&](auto fix_tag) {
+                    constexpr bool kFix = decltype(fix_tag)::value;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int q = q8 + kk;
+                        const int jj = width - 1 - q + (31 - t);
+                        const T src = (t == 0) ? si8[kk] : s_prev;
+                        const T s_in = __shfl_sync(kFull, src, (t + 1) & 31);
+                        // branch-free step: inactive lanes write the dummy row
+                        const bool act = jj >= 0 && jj < width;
+                        const bool cell = act && row_ok;
+                        const int jc = act ? jj : 32;
+                        T e = fma(e_right, pl_right, s_in);
+                        e = e < T(1) ? e : T(1);
+                        if constexpr (kFix) {
+                            const int j = j0 + jj;
+                            e = (i == a.N && j == a.M) ? T(1) : e;
+                            e = in_band(i, j, a.bw) ? e : T(0);
+                        }
+                        e = cell ? e : T(0);
+                        const T s_out = cell ? fma(e, pu8[kk], e_right * pd_right) : s_prev;
+                        e_right = cell ? e : e_right;
+                        pl_right = cell ? pl8[kk] : pl_right;
+                        pd_right = cell ? pd8[kk] : pd_right;
+                        et_s[t * 34 + jc] = e;
+                        if (t == 0) sout_s[jc] = s_out;
+                        s_prev = s_out;
+                        // lane 0 has now completed done + 1 columns: a full group
+                        // of 8 ends at kk = 6 (q = 31 + 8 g + 7)
+                        if (kk == 6) publish(q - 31);
+                    }
+                };
+                if (has_end_tile || a.bw != 0) esteps(std::true_type{});
+                else esteps(std::false_type{});
+                publish(min(q8 + 7 - 31, width - 1));
             }
             __syncwarp();
+            lap(2);
             // final status: does any S go up?  (stops the spread of hints over
             // tiles whose inputs turned out to be exactly zero)
             const bool s_nz = __any_sync(kFull, t < width && sout_s[t] != T(0));
@@ -374,14 +524,24 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
             }
             }
             __syncwarp();
+            lap(4);
             advance(c);
             ++ntiles;
             --c;
         }
+        lap(5);
+        if (A.trace && t == 0)
+            for (int e = 0; e < 6; ++e)
+                A.trace[32 * (size_t)a.B * a.S + 8 * ((size_t)b * a.S + s) + e] = (unsigned long long)cyc[e];
         if (A.trace && t == 0) {
             A.trace[2 * ((size_t)a.B * a.S + (size_t)b * a.S + s) + 1] = global_ns();
             A.trace[4 * (size_t)a.B * a.S + (size_t)b * a.S + s] = (unsigned long long)ntiles;
         }
+    }
+    if constexpr (kTc) {
+        tc::tc_fence_before();
+        __syncwarp();
+        tc::tmem_dealloc<128>(tmem);
     }
 }
 

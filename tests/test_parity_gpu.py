@@ -122,13 +122,25 @@ def test_fused_equals_unfused_bitwise(engine):
         assert np.array_equal(u, v)
 
 
-def test_fused_matches_unfused_f32(engine):
-    x, y = _bench_like(3, 75, 16, seed=3)
-    a = engine.sdtw_with_gradients(x, y, 0.3)
-    b = engine.sdtw_with_gradients(x, y, 0.3, fused=True)
-    assert rel_err(a[0], b[0]).max() <= 1e-6
-    for u, v in zip(a[1:], b[1:]):
-        assert grad_stats(u, v)[0] <= 1e-4
+@pytest.mark.parametrize("B,N,M,D,gamma,bw", [
+    (3, 75, 75, 16, 0.3, 0),      # ragged strips and chunks, D padded to 64
+    (2, 300, 170, 128, 0.1, 0),   # N > M tail, 3 super-strips, partial last one
+    (2, 130, 333, 100, 1.0, 0),   # M > N tail, D not a multiple of 16
+    (4, 256, 256, 64, 0.05, 40),  # Sakoe-Chiba band
+    (1, 33, 1, 8, 1.0, 0),        # single column
+    (1, 1, 40, 8, 1.0, 0),        # single row
+])
+def test_fused_tc_equals_unfused_bitwise_f32(engine, B, N, M, D, gamma, bw):
+    """fp32 fused mode (tcgen05 costs inside the DP kernels) reproduces the
+    unfused mode (tcgen05 cost tensor) bit for bit: same operand split, same
+    MMA sequence, same epilogue (test_backward.cpp:225-241 analogue)."""
+    rng = np.random.default_rng(B * 1000 + N + M + D)
+    x = rng.standard_normal((B, N, D)).astype(np.float32)
+    y = rng.standard_normal((B, M, D)).astype(np.float32)
+    a = engine.sdtw_with_gradients(x, y, gamma, bandwidth=bw)
+    b = engine.sdtw_with_gradients(x, y, gamma, bandwidth=bw, fused=True)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
 
 
 def test_deterministic(engine):
