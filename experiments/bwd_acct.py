@@ -9,6 +9,7 @@ fused = len(sys.argv) > 2 and sys.argv[2] == "fused"
 B, L, D = cfg["B"], cfg["L"], cfg["D"]
 S = (L + 31) // 32
 eng = Engine(0)
+torch.manual_seed(0)
 x = torch.randn((B, L, D), device="cuda"); y = torch.randn((B, L, D), device="cuda")
 tr = torch.zeros(40 * B * S, dtype=torch.int64, device="cuda")
 eng.enable_timing(True)
@@ -22,11 +23,11 @@ for it in range(3):
         ph = eng.phase_times()
 eng.lib.sdtw_debug_set_trace(eng.ctx, None)
 t = tr.cpu().numpy().astype(np.float64)
-cy = t[32 * B * S:40 * B * S].reshape(B, S, 8)[..., :6]
+cy = t[32 * B * S:40 * B * S].reshape(B, S, 8)
 nt = t[4 * B * S:5 * B * S].reshape(B, S)
-names = ["recompute", "S-wait", "E-steps", "status-wait", "tile-epilogue", "other"]
+names = ["recompute", "S-wait", "E-steps", "status-wait", "tile-epilogue", "other", "tc-stage+epi", "tc-mma"]
 print(sys.argv[1], "fused" if fused else "unfused", {k: round(v, 3) for k, v in ph.items()})
-med = np.median(cy.reshape(-1, 6), axis=0)
+med = np.median(cy.reshape(-1, 8), axis=0)
 print("  per strip (median, kcycles):", dict(zip(names, [round(float(v) / 1e3, 1) for v in med])),
       "live tiles/strip %.2f" % nt.mean())
 tot = cy.sum(axis=(0, 1))

@@ -5,6 +5,7 @@ import numpy as np, torch
 from paper_2602_17206_b200 import Engine
 B, N, M, D = (int(v) for v in (sys.argv[1:5] if len(sys.argv) > 4 else (32, 4096, 4096, 128)))
 eng = Engine(0)
+torch.manual_seed(0)
 S = (N + 31) // 32
 x = torch.randn((B, N, D), device="cuda"); y = torch.randn((B, M, D), device="cuda")
 tr = torch.zeros(32 * B * S, dtype=torch.int64, device="cuda")

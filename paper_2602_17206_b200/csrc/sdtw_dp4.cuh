@@ -98,7 +98,7 @@ __device__ __forceinline__ T bwd_cost(const DpArgs<T> &a, const T *ring, int b, 
 // is warp 0 of its CTA, so it owns TMEM lanes 0..31: its strip's 32 rows are
 // rows 0..31 of an M = 128 MMA whose other rows are don't-care.
 template <class T, bool kFused, bool kTc = false>
-__global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsigned long long *stat,
+__global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, unsigned long long *stat,
                                                             FusedTcArgs F)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
         int ntiles = 0;
         // cycle accounting (trace mode): [32 B S + 8 (b S + s) + e]: e = 0
         // recompute, 1 S wait, 2 E steps, 3 status waits, 4 tile epilogue, 5 other
-        long long cyc[6] = {0, 0, 0, 0, 0, 0};
+        long long cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         long long c_mark = A.trace ? clock64() : 0;
         auto lap = [&](int e) {
             if (A.trace) {
@@ -183,19 +183,53 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                 uint8_t *stage = reinterpret_cast<uint8_t *>(base);
                 const uint32_t idesc = tc::idesc_f16_f32(128, 32);
                 const SplitScale sc = split_scale(A.absmax);
+                // raw fp32 staging after the three fp16 operand tiles (the
+                // probability slots, E tile and ring are all free until the
+                // recompute loop / epilogue)
+                lap(5);
+                // column norms of the (up to) three chunks, loaded first
+                float yv3[3];
+#pragma unroll
+                for (int z = 0; z < 3; ++z) {
+                    const int jz = 32 * (cr - z) + t;
+                    yv3[z] = (z < nt && jz < a.M) ? (float)a.yn[(size_t)b_ * a.M + jz] : 0.f;
+                }
+                float *raw = reinterpret_cast<float *>(stage + 3 * 8192);
+                const bool async_ok = (a.D & 3) == 0;
+                const float *xg = reinterpret_cast<const float *>(a.x) + (size_t)b_ * a.N * a.D;
+                const float *yg = reinterpret_cast<const float *>(a.y) + (size_t)b_ * a.M * a.D;
                 if (!xl) {
-                    stage_split_rows(reinterpret_cast<const float *>(a.x) + (size_t)b_ * a.N * a.D, a.D, 32 * s_, 32, a.N,
-                                     a.D, dpad, sc.sx, xs, t);
+                    if (async_ok) {
+                        raw_rows_async(raw, xg, a.D, 32 * s_, 32, a.N, 0, dpad, a.D, t);
+                        cp_async_commit();
+                        cp_async_wait<0>();
+                        __syncwarp();
+                        split_raw_rows(raw, 32, dpad, sc.sx, xs, xs + 32 * dpad * 2, 0, 512, t);
+                        __syncwarp();
+                    } else {
+                        stage_split_rows(xg, a.D, 32 * s_, 32, a.N, a.D, dpad, sc.sx, xs, t);
+                    }
                     xl = true;
                 }
                 for (int kh = 0; kh < dpad / 64; ++kh) {
                     // y chunks cr - z, features [64 kh, 64 kh + 64): 32 rows x 64
-                    for (int z = 0; z < nt; ++z)
-                        stage_split_rows(reinterpret_cast<const float *>(a.y) + (size_t)b_ * a.M * a.D +
-                                             (size_t)64 * kh,
-                                         a.D, 32 * (cr - z), 32, a.M, a.D - 64 * kh, 64, sc.sy, stage + z * 8192, t);
+                    if (async_ok) {
+                        for (int z = 0; z < nt; ++z)
+                            raw_rows_async(raw + z * 32 * 68, yg, a.D, 32 * (cr - z), 32, a.M, 64 * kh, 64, a.D, t);
+                        cp_async_commit();
+                        cp_async_wait<0>();
+                        __syncwarp();
+                        for (int z = 0; z < nt; ++z)
+                            split_raw_rows(raw + z * 32 * 68, 32, 64, sc.sy, stage + z * 8192, stage + z * 8192 + 4096, 0,
+                                           512, t);
+                    } else {
+                        for (int z = 0; z < nt; ++z)
+                            stage_split_rows(yg + (size_t)64 * kh, a.D, 32 * (cr - z), 32, a.M, a.D - 64 * kh, 64, sc.sy,
+                                             stage + z * 8192, t);
+                    }
                     tc::fence_async_smem();
                     __syncwarp();
+                    lap(6);
                     tc::tc_fence_after();
                     if (t == 0) {
                         const uint32_t xh = tc::smem_u32(xs), xlo = xh + 32u * dpad * 2;
@@ -217,12 +251,13 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                     tc::mbar_wait(&tc_bar[0], tc_ph[0]);
                     tc_ph[0] ^= 1u;
                     tc::tc_fence_after();
+                    lap(7);
                 }
                 for (int z = 0; z < nt; ++z) {
                     float acc[32];
                     tc::tmem_ld32(tmem + 32u * z, acc);
                     const int j0 = 32 * (cr - z);
-                    const float yv = (j0 + t < a.M) ? (float)a.yn[(size_t)b_ * a.M + j0 + t] : 0.f;
+                    const float yv = z == 0 ? yv3[0] : (z == 1 ? yv3[1] : yv3[2]);
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         const float yj = __shfl_sync(kFull, yv, e);
@@ -233,6 +268,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
                     }
                 }
                 tc::tc_fence_before();
+                lap(6);
             }
         };
         // recompute tile cr and, speculatively, cr-1 and cr-2 (independent
@@ -264,35 +300,56 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
             // tiles touching row 1, column 1 or a band edge take the general
             // cell; all others a branch-free one (warp-uniform choice)
             const bool fix = (s == 0) || (cr - nt + 1 <= 1) || (a.bw != 0);
-            for (int q = 0; q < 32 + 31; ++q) {
-                T src[3], u[3];
+            // 8-step sub-groups (64 steps; the last is a no-op): costs and top
+            // halos of the sub-group loaded up front, branch-free steps
+            for (int q8 = 0; q8 < 64; q8 += 8) {
+                T d8[3][8], hs8[3][8];
 #pragma unroll
-                for (int z = 0; z < 3; ++z) src[z] = (t == 31) ? halo_s[z * 32 + (q & 31)] : hp[z];
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int q = q8 + kk;
 #pragma unroll
-                for (int z = 0; z < 3; ++z) u[z] = __shfl_sync(kFull, src[z], (t + 31) & 31);
-                const int jj = q - t;
-#pragma unroll
-                for (int z = 0; z < 3; ++z) {
-                    const int wz = z == 0 ? wr : 32;
-                    const bool act = z < nt && row_ok && jj >= 0 && jj < wz;
-                    const int j = 32 * (cr - z) + 1 + jj;
-                    const T d = kFused ? (act ? bwd_cost<T, kFused>(a, ring, b, s, t, i, j) : T(0))
-                                       : bwd_cost<T, kFused>(a, ring, b, s, t, i, j);
-                    T v, h, pd, pu, pl;
-                    if (fix) {
-                        const Cell<T> cc = dp_cell<T, true>(i, j, a.bw, d, u[z], lc[z], a.k, a.gln2);
-                        v = cc.v; h = cc.h; pd = cc.pd; pu = cc.pu; pl = cc.pl;
-                    } else {
-                        prob_cell<T>(d, u[z], lc[z], a.k, a.gln2, v, h, pd, pu, pl);
+                    for (int z = 0; z < 3; ++z) {
+                        hs8[z][kk] = halo_s[z * 32 + (q & 31)];
+                        // skewed row 32 (cr - z) + q of the ring
+                        d8[z][kk] = kFused ? T(0) : ring[((cr - z + (q >> 5)) & 3) * 1024 + (q & 31) * 32 + t];
                     }
-                    // inactive lanes write the dummy row: no divergent branch
-                    T *Pz = base + kSlot * z + (act ? jj : 32) * 32 + t;
-                    Pz[0] = pd;
-                    Pz[1056] = pu;
-                    Pz[2112] = pl;
-                    lc[z] = act ? v : lc[z];
-                    hp[z] = act ? h : hp[z];
                 }
+                auto rsteps = [&](auto fix_tag) {
+                    constexpr bool kFix = decltype(fix_tag)::value;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int q = q8 + kk;
+                        T src[3], u[3];
+#pragma unroll
+                        for (int z = 0; z < 3; ++z) src[z] = (t == 31) ? hs8[z][kk] : hp[z];
+#pragma unroll
+                        for (int z = 0; z < 3; ++z) u[z] = __shfl_sync(kFull, src[z], (t + 31) & 31);
+                        const int jj = q - t;
+#pragma unroll
+                        for (int z = 0; z < 3; ++z) {
+                            const int wz = z == 0 ? wr : 32;
+                            const bool act = z < nt && row_ok && jj >= 0 && jj < wz;
+                            const int j = 32 * (cr - z) + 1 + jj;
+                            const T d = kFused ? (act ? bwd_cost<T, kFused>(a, ring, b, s, t, i, j) : T(0)) : d8[z][kk];
+                            T v, h, pd, pu, pl;
+                            if constexpr (kFix) {
+                                const Cell<T> cc = dp_cell<T, true>(i, j, a.bw, d, u[z], lc[z], a.k, a.gln2);
+                                v = cc.v; h = cc.h; pd = cc.pd; pu = cc.pu; pl = cc.pl;
+                            } else {
+                                prob_cell<T>(d, u[z], lc[z], a.k, a.gln2, v, h, pd, pu, pl);
+                            }
+                            // inactive lanes write the dummy row: no divergent branch
+                            T *Pz = base + kSlot * z + (act ? jj : 32) * 32 + t;
+                            Pz[0] = pd;
+                            Pz[1056] = pu;
+                            Pz[2112] = pl;
+                            lc[z] = act ? v : lc[z];
+                            hp[z] = act ? h : hp[z];
+                        }
+                    }
+                };
+                if (fix) rsteps(std::true_type{});
+                else rsteps(std::false_type{});
             }
             __syncwarp();
             lap(0);
@@ -531,7 +588,7 @@ __global__ void __launch_bounds__(32) sdtw_backward4_kernel(Dp3Args<T> A, unsign
         }
         lap(5);
         if (A.trace && t == 0)
-            for (int e = 0; e < 6; ++e)
+            for (int e = 0; e < 8; ++e)
                 A.trace[32 * (size_t)a.B * a.S + 8 * ((size_t)b * a.S + s) + e] = (unsigned long long)cyc[e];
         if (A.trace && t == 0) {
             A.trace[2 * ((size_t)a.B * a.S + (size_t)b * a.S + s) + 1] = global_ns();

@@ -77,6 +77,72 @@ __device__ __forceinline__ void stage_split_rows(const float *__restrict__ src, 
     }
 }
 
+// 8 floats (scaled by sc) -> fp16 hi and lo halves, two per conversion
+// instruction; the same round-to-nearest values as split_store8.
+__device__ __forceinline__ void split8_packed(const float (&f)[8], float sc, uint4 &hq, uint4 &lq)
+{
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 v = make_float2(f[2 * e] * sc, f[2 * e + 1] * sc);
+        const __half2 h2 = __float22half2_rn(v);
+        const float2 hb = __half22float2(h2);
+        const __half2 l2 = __float22half2_rn(make_float2(v.x - hb.x, v.y - hb.y));
+        hw[e] = *reinterpret_cast<const uint32_t *>(&h2);
+        lw[e] = *reinterpret_cast<const uint32_t *>(&l2);
+    }
+    hq = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    lq = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
+// Asynchronous variant for one warp: raw fp32 rows land in shared memory by
+// cp.async (zero-filled past row R / feature D; needs D % 4 == 0), then are
+// split shared -> shared.  raw: rows x (kc + 4) floats (padded stride: the
+// per-row 32-byte reads of the split are bank-conflict free).
+__device__ __forceinline__ void cp_async16_zfill(void *smem_dst, const void *gmem_src, int src_bytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gmem_src), "r"(src_bytes)
+                 : "memory");
+}
+// issue: rows [r0, r0 + rows) x features [k0, k0 + kc) of src[R][ld] (valid D)
+__device__ __forceinline__ void raw_rows_async(float *raw, const float *__restrict__ src, int ld, int r0, int rows, int R,
+                                               int k0, int kc, int D, int lane)
+{
+    const int pieces = kc / 4;
+    for (int u = lane; u < rows * pieces; u += 32) {
+        const int r = u / pieces, pc = u % pieces;
+        const int row = r0 + r, k = k0 + 4 * pc;
+        const int nb = row < R ? max(0, min(16, (D - k) * 4)) : 0;
+        const float *p = src + (size_t)min(row, R - 1) * ld + min(k, D - 4);
+        cp_async16_zfill(raw + r * (kc + 4) + 4 * pc, p, nb);
+    }
+}
+// split: raw rows [0, rows) -> operand tile rows [row0, row0 + rows), K blocks
+// [0, kc / 8) (K-block stride kbs bytes), hi at `hi`, lo at `lo`
+__device__ __forceinline__ void split_raw_rows(const float *raw, int rows, int kc, float sc, uint8_t *hi, uint8_t *lo,
+                                               int row0, int kbs, int lane)
+{
+    const int kbn = kc / 8;
+    for (int u = lane; u < rows * kbn; u += 32) {
+        const int r = u % rows, kb = u / rows;
+        const float4 a4 = *reinterpret_cast<const float4 *>(raw + r * (kc + 4) + 8 * kb);
+        const float4 b4 = *reinterpret_cast<const float4 *>(raw + r * (kc + 4) + 8 * kb + 4);
+        const float f[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
+        __align__(16) __half hh[8];
+        __align__(16) __half ll[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float v = f[e] * sc;
+            hh[e] = __float2half_rn(v);
+            ll[e] = __float2half_rn(v - __half2float(hh[e]));
+        }
+        const uint32_t off = tc::kmajor_off(row0 + r, kb, kbs);
+        *reinterpret_cast<uint4 *>(hi + off) = *reinterpret_cast<const uint4 *>(hh);
+        *reinterpret_cast<uint4 *>(lo + off) = *reinterpret_cast<const uint4 *>(ll);
+    }
+}
+
 // The cost epilogue shared by all tensor-core paths (cost_gemm_tc_kernel's):
 // row i, column j (0-based), accumulator acc.
 __device__ __forceinline__ float tc_cost(float acc, float xi, float yj, float m2, bool ok)
@@ -189,17 +255,11 @@ __device__ __forceinline__ void half_chunk_store(const HalfChunk &h, float sc, u
         if (kb < kbn) {
             const float f[8] = {h.v[i][0].x, h.v[i][0].y, h.v[i][0].z, h.v[i][0].w,
                                 h.v[i][1].x, h.v[i][1].y, h.v[i][1].z, h.v[i][1].w};
-            __align__(16) __half hh[8];
-            __align__(16) __half ll[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float v = f[e] * sc;
-                hh[e] = __float2half_rn(v);
-                ll[e] = __float2half_rn(v - __half2float(hh[e]));
-            }
+            uint4 hq, lq;
+            split8_packed(f, sc, hq, lq);
             const uint32_t off = tc::kmajor_off(row0 + r, kb, kbs);
-            *reinterpret_cast<uint4 *>(hi + off) = *reinterpret_cast<const uint4 *>(hh);
-            *reinterpret_cast<uint4 *>(lo + off) = *reinterpret_cast<const uint4 *>(ll);
+            *reinterpret_cast<uint4 *>(hi + off) = hq;
+            *reinterpret_cast<uint4 *>(lo + off) = lq;
         }
     }
 }
