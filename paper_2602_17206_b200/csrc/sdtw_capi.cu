@@ -13,6 +13,7 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -29,6 +30,7 @@
 #include "sdtw_dp3.cuh"
 #include "sdtw_dp4.cuh"
 #include "sdtw_fused.cuh"
+#include "sdtw_grad.cuh"
 #include "sdtw_tc.cuh"
 
 namespace {
@@ -447,22 +449,6 @@ struct Pipeline {
         return (unsigned)std::max(1, std::min(need, occ * ctx->sm_count));
     }
 
-    template <int K>
-    void launch_forward()
-    {
-        auto a = args();
-        const int threads = 128;
-        if (fused) {
-            auto kern = sdtw::sdtw_forward2_kernel<T, K, true>;
-            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, true>::kPerWarp * sizeof(T);
-            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, a);
-        } else {
-            auto kern = sdtw::sdtw_forward2_kernel<T, K, false>;
-            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, false>::kPerWarp * sizeof(T);
-            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, a);
-        }
-    }
-
     using Ent = typename sdtw::Tagged<T>::Ent;
     Ent *hbt = nullptr, *sbt = nullptr;
     unsigned long long *stat = nullptr;
@@ -470,7 +456,8 @@ struct Pipeline {
     Buf<long long> gx_fx, gy_fx, rs_fx, cs_fx;
     Buf<T> tiles;
     Buf<int4> tile_meta;
-    unsigned tile_cap = 0;
+    Buf<int> strip_tiles;
+    int tile_quota = 0;
     Buf<unsigned> stats;
 
     void halos()
@@ -512,7 +499,8 @@ struct Pipeline {
         A.absmax = absmax.p;
         A.tiles = tiles.p;
         A.tile_meta = tile_meta.p;
-        A.tile_cap = tile_cap;
+        A.strip_tiles = strip_tiles.p;
+        A.tile_quota = tile_quota;
         A.stats = stats.p;
         A.trace = ctx->trace;
         return A;
@@ -574,23 +562,36 @@ struct Pipeline {
     // B x N x M alignment gradient in E.
     void backward(T *gx, T *gy, bool want_E)
     {
-        gx_fx = Buf<long long>(ctx, (size_t)B * N * D);
-        gy_fx = Buf<long long>(ctx, (size_t)B * M * D);
-        rs_fx = Buf<long long>(ctx, (size_t)B * N);
-        cs_fx = Buf<long long>(ctx, (size_t)B * M);
-        CUDA_OK(cudaMemsetAsync(gx_fx.p, 0, gx_fx.n * 8, ctx->stream));
-        CUDA_OK(cudaMemsetAsync(gy_fx.p, 0, gy_fx.n * 8, ctx->stream));
-        CUDA_OK(cudaMemsetAsync(rs_fx.p, 0, rs_fx.n * 8, ctx->stream));
-        CUDA_OK(cudaMemsetAsync(cs_fx.p, 0, cs_fx.n * 8, ctx->stream));
-        // compact tile store: all tiles when small, else 1/8 of them (the rest
-        // is contracted in the backward's own warp)
-        const size_t all_tiles = (size_t)B * S * C;
-        size_t cap = all_tiles;
-        if (all_tiles * 1024 * sizeof(T) > ((size_t)64 << 20)) cap = std::max<size_t>(all_tiles / 8, 16384);
-        cap = std::min(cap, all_tiles);
-        tile_cap = (unsigned)cap;
+        // compact store of the non-zero E tiles: a quota of slots per strip,
+        // every chunk when the store fits 512 MiB, else as many as fit (>= 8);
+        // only a quota below C needs the fixed-point accumulators of the
+        // in-warp overflow contraction (sdtw_grad.cuh)
+        const size_t strips = (size_t)B * S;
+        size_t quota = std::max<size_t>(8, ((size_t)512 << 20) / (strips * 1024 * sizeof(T)));
+        quota = std::min<size_t>(quota, (size_t)C);
+        if (const char *e = std::getenv("SDTW_DEBUG_TILE_QUOTA"))  // test hook: force the overflow path
+            quota = std::max<size_t>(1, std::min<size_t>(quota, std::strtoull(e, nullptr, 10)));
+        tile_quota = (int)quota;
+        const size_t cap = strips * quota;
+        const bool need_fx = quota < (size_t)C;
+        if (need_fx) {
+            gx_fx = Buf<long long>(ctx, (size_t)B * N * D);
+            gy_fx = Buf<long long>(ctx, (size_t)B * M * D);
+            rs_fx = Buf<long long>(ctx, (size_t)B * N);
+            cs_fx = Buf<long long>(ctx, (size_t)B * M);
+            CUDA_OK(cudaMemsetAsync(gx_fx.p, 0, gx_fx.n * 8, ctx->stream));
+            CUDA_OK(cudaMemsetAsync(gy_fx.p, 0, gy_fx.n * 8, ctx->stream));
+            CUDA_OK(cudaMemsetAsync(rs_fx.p, 0, rs_fx.n * 8, ctx->stream));
+            CUDA_OK(cudaMemsetAsync(cs_fx.p, 0, cs_fx.n * 8, ctx->stream));
+        } else {
+            gx_fx = Buf<long long>();
+            gy_fx = Buf<long long>();
+            rs_fx = Buf<long long>();
+            cs_fx = Buf<long long>();
+        }
         tiles = Buf<T>(ctx, cap * 1024);
         tile_meta = Buf<int4>(ctx, cap);
+        strip_tiles = Buf<int>(ctx, strips);
         if (want_E) {
             E = Buf<T>(ctx, (size_t)B * N * M);
             CUDA_OK(cudaMemsetAsync(E.p, 0, (size_t)B * N * M * sizeof(T), ctx->stream));
@@ -618,16 +619,34 @@ struct Pipeline {
                 LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat, sdtw::FusedTcArgs{});
             }
         }
-        {
+        if (gx || gy) {
+            // ordered, atomic-free contraction of the stored tiles
             Phase ph(ctx, 4);
-            LAUNCH(ctx, sdtw::tile_contract_kernel<T>, (unsigned)(ctx->sm_count * 4),
-                   32 * sdtw::contract_warps<T>(), 0, A);
+            const int ns = B * S, nc = B * C;
+            const unsigned cg = (unsigned)ctx->sm_count * 8;
             if (gx)
-                LAUNCH(ctx, sdtw::finalize_grads_fx_kernel<T>, grid_for((size_t)B * N * D, 256), 256, 0, x,
-                       rs_fx.p, gx_fx.p, absmax.p, N, M, B * N, D, 0, gx);
-            if (gy)
-                LAUNCH(ctx, sdtw::finalize_grads_fx_kernel<T>, grid_for((size_t)B * M * D, 256), 256, 0, y,
-                       cs_fx.p, gy_fx.p, absmax.p, N, M, B * M, D, 1, gy);
+                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(ns, cg), 256, 0, tiles.p,
+                       tile_meta.p, strip_tiles.p, tile_quota, nullptr, nullptr, 0, B, S, C, N, M, D, x, y, gx);
+            if (gy) {
+                Buf<int> cnt(ctx, (size_t)nc), off(ctx, (size_t)nc + 1), ord(ctx, cap);
+                CUDA_OK(cudaMemsetAsync(cnt.p, 0, cnt.n * sizeof(int), ctx->stream));
+                const unsigned tg = grid_for(cap, 256, (unsigned)ctx->sm_count * 8);
+                LAUNCH(ctx, sdtw::tile_hist_kernel, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C, cnt.p);
+                LAUNCH(ctx, sdtw::exclusive_scan_kernel, 1, 1024, 0, cnt.p, nc, off.p);
+                LAUNCH(ctx, sdtw::tile_scatter_kernel, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C,
+                       off.p, cnt.p, ord.p);
+                LAUNCH(ctx, sdtw::segment_sort_kernel, grid_for(nc, 128), 128, 0, off.p, ord.p, tile_meta.p, nc);
+                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(nc, cg), 256, 0, tiles.p,
+                       tile_meta.p, strip_tiles.p, tile_quota, off.p, ord.p, 1, B, S, C, N, M, D, y, x, gy);
+            }
+            if (need_fx) {
+                if (gx)
+                    LAUNCH(ctx, sdtw::finalize_grads_fx_add_kernel<T>, grid_for((size_t)B * N * D, 256), 256, 0, x,
+                           rs_fx.p, gx_fx.p, absmax.p, N, M, B * N, D, 0, gx);
+                if (gy)
+                    LAUNCH(ctx, sdtw::finalize_grads_fx_add_kernel<T>, grid_for((size_t)B * M * D, 256), 256, 0, y,
+                           cs_fx.p, gy_fx.p, absmax.p, N, M, B * M, D, 1, gy);
+            }
         }
         // the cost tensor is dropped after the backward (backward.hpp:291)
         dsk = Buf<T>();

@@ -18,12 +18,12 @@
 //    of tiles are exactly zero on N(0,1) data.
 //
 //  * Input gradients without the dense E: the backward queues each non-zero
-//    E tile (4 KB) in a compact store; tile_contract_kernel contracts them
-//    with the tile's y rows (grad_x) and x rows (grad_y) plus both marginals
-//    into 64-bit fixed-point accumulators (integer atomics are associative,
-//    so the result is bit-identical for any schedule), and
-//    finalize_grads_fx_kernel applies grad = 2 (x * marginal - acc)
-//    (backward.hpp:208-266).  E reaches HBM only if the caller asks for it.
+//    E tile (4 KB) in a compact store, contracted in a fixed order by
+//    sdtw_grad.cuh (backward.hpp:208-266).  If a capped store overflows, the
+//    backward contracts the remaining tiles itself (tile_contract_fx) into
+//    64-bit fixed-point accumulators (integer atomics are associative, so the
+//    result is bit-identical for any schedule).  E reaches HBM only if the
+//    caller asks for it.
 #pragma once
 #include "sdtw_common.cuh"
 #include "sdtw_dp.cuh"
@@ -112,10 +112,14 @@ struct Dp3Args {
     long long *gx_fx, *gy_fx;      // [B][N][D] sum_j E y_j,  [B][M][D] sum_i E x_i
     long long *rs_fx, *cs_fx;      // [B][N] row marginals, [B][M] column marginals
     const unsigned *absmax;        // [0] max|x|, [1] max|y| (fp32 bit patterns)
-    // compact store of non-zero E tiles for the contraction kernel
-    T *tiles;                      // [cap][32][32]
-    int4 *tile_meta;               // [cap] (b, s, c, width)
-    unsigned tile_cap;
+    // compact store of non-zero E tiles for the contraction (sdtw_grad.cuh):
+    // strip (b, s) owns slots [(b S + s) quota, +quota), filled in its
+    // processing order (chunks right to left); tiles past the quota are
+    // contracted by the backward itself into the fixed-point accumulators
+    T *tiles;                      // [B S quota][32][32]
+    int4 *tile_meta;               // [B S quota] (b, s, c, width)
+    int *strip_tiles;              // [B S] tiles stored per strip
+    int tile_quota;
     unsigned *stats;               // [0] live tiles, [1] tiles stored, [2] overflow (in-warp)
     unsigned long long *trace;     // optional [B*S][2] %globaltimer at strip start / end (forward)
 };
@@ -420,11 +424,8 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
 }
 
 // --------------------------------------------------------------------------
-// Backward v3
+// Gradient contraction of the backward's non-zero E tiles
 // --------------------------------------------------------------------------
-template <class T, bool kFused>
-using Bwd3Smem = Bwd2Smem<T, kFused>;
-
 // Contraction of one non-zero E tile (32 x 32, [r][jj] in shared memory):
 //   gx[i0+r][k] += sum_jj E[r][jj] y[j0+jj][k],  gy[j0+jj][k] += sum_r E[r][jj] x[i0+r][k]
 // plus both marginals, into the fixed-point accumulators.  One warp; lane =
@@ -471,195 +472,6 @@ __device__ __forceinline__ void tile_contract_fx(const Dp3Args<T> &A, const FxSc
                 for (int q = 0; q < 32; ++q)
                     if (q < kn) fx_add(dst + q, (double)acc[q], sc);
             }
-        }
-    }
-}
-
-// Contraction kernel over the compact store of non-zero tiles (one warp per
-// tile, grid-stride over the stored count).
-template <class T>
-constexpr int contract_warps() { return sizeof(T) == 4 ? 4 : 2; }
-
-template <class T>
-__global__ void __launch_bounds__(128) tile_contract_kernel(Dp3Args<T> A)
-{
-    constexpr int W = contract_warps<T>();
-    __shared__ T et_s[W][32 * 32];
-    __shared__ T stage[W][32 * 33];
-    const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
-    const unsigned n = min(A.stats[1], A.tile_cap);
-    const FxScales fx = fx_scales(A.absmax, A.a.N, A.a.M);
-    for (unsigned slot = blockIdx.x * W + w; slot < n; slot += gridDim.x * W) {
-        const int4 m = A.tile_meta[slot];
-        const T *src = A.tiles + (size_t)slot * 1024;
-        for (int r = 0; r < 32; ++r) et_s[w][r * 32 + t] = src[r * 32 + t];
-        __syncwarp();
-        tile_contract_fx<T>(A, fx, m.x, m.y, m.z, m.w, et_s[w], stage[w], t);
-        __syncwarp();
-    }
-}
-
-// grad = 2 (v * marginal - acc)  (backward.hpp:227-263) from the fixed-point
-// accumulators.
-template <class T>
-__global__ void finalize_grads_fx_kernel(const T *__restrict__ v, const long long *__restrict__ marg_fx,
-                                         const long long *__restrict__ acc_fx, const unsigned *absmax, int N,
-                                         int M, int rows, int D, int which, T *__restrict__ grad)
-{
-    const FxScales fx = fx_scales(absmax, N, M);
-    const double sm = 1.0 / (which == 0 ? fx.rs : fx.cs);
-    const double sa = 1.0 / (which == 0 ? fx.gx : fx.gy);
-    const size_t total = (size_t)rows * D;
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t r = idx / D;
-        const T marg = (T)((double)marg_fx[r] * sm);
-        const T acc = (T)((double)acc_fx[idx] * sa);
-        grad[idx] = T(2) * (v[idx] * marg - acc);
-    }
-}
-
-template <class T, bool kFused>
-__global__ void __launch_bounds__(128) sdtw_backward3_kernel(Dp3Args<T> A)
-{
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    const DpArgs<T> &a = A.a;
-    using SM = Bwd3Smem<T, kFused>;
-    using TG = Tagged<T>;
-    const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
-    T *base = reinterpret_cast<T *>(smem_raw) + w * SM::kPerWarp;
-    T *pd_s = base, *pu_s = base + 1024, *pl_s = base + 2048;
-    T *et_s = base + SM::kP;
-    T *ring = et_s + SM::kE;
-    T *halo_s = ring + SM::kRing;
-    T *sio_s = halo_s + 32;
-    const unsigned epoch = A.epoch;
-    const int total = a.B * a.S;
-    const FxScales fx = fx_scales(A.absmax, a.N, a.M);
-    for (;;) {
-        const unsigned tk = warp_ticket(&a.tickets[1]);
-        if ((int)tk >= total) return;
-        const int s = a.S - 1 - (int)tk / a.B, b = (int)tk % a.B;
-        const int i = 32 * s + t + 1;
-        const bool row_ok = i <= a.N;
-        const T *dsrc = kFused ? nullptr : a.dsk + ((size_t)b * a.S + s) * (size_t)a.KK * 32;
-        const int ngroups_row = a.KK / 32;
-        T e_right = T(0), pl_right = T(0), pd_right = T(0);
-        for (int c = a.C - 1; c >= 0; --c) {
-            const int j0 = 32 * c + 1;
-            const int width = min(32, a.M - 32 * c);
-            const bool has_end = (s == a.S - 1) && (c == a.C - 1);
-            // A tile is live if E enters it from the right (known now) or from
-            // below (known once the strip below published this chunk).  When
-            // the right side is live, recompute first and poll afterwards.
-            const bool live_right = __any_sync(kFull, e_right != T(0)) || has_end;
-            T sbv = T(0);
-            bool polled = false;
-            if (!live_right) {
-                if (s < a.S - 1)
-                    sbv = poll_entries<T>(A.sbt + ((size_t)b * a.S + (s + 1)) * a.M + (j0 - 1), width, epoch, t);
-                polled = true;
-                if (!__any_sync(kFull, sbv != T(0))) {
-                    if (t < width) TG::store(A.sbt + ((size_t)b * a.S + s) * a.M + (j0 - 1) + t, T(0), epoch);
-                    pl_right = T(0);
-                    pd_right = T(0);
-                    continue;  // every E of this tile is exactly 0
-                }
-            }
-            if (!kFused) {
-                for (int g = c; g <= c + 1; ++g)
-                    if (g < ngroups_row) load_group(ring + (g % 3) * 1024, dsrc + (size_t)g * 1024, t);
-                cp_async_commit();
-            }
-            T l_carry = (c > 0 && row_ok) ? a.vc[((size_t)b * a.C + (c - 1)) * a.N + (i - 1)] : T(0);
-            halo_s[t] = (s > 0 && t < width) ? TG::value(A.hbt + ((size_t)b * a.S + (s - 1)) * a.M + (j0 - 1) + t)
-                                             : T(0);
-            if (!kFused) cp_async_wait<0>();
-            __syncwarp();
-            // ---- phase R: recompute the tile's forward -> probabilities ----
-            T h_prev = T(0);
-            for (int q = 0; q < width + 31; ++q) {
-                const T src = (t == 31) ? halo_s[q < width ? q : 0] : h_prev;
-                const T u = __shfl_sync(kFull, src, (t + 31) & 31);
-                const int jj = q - t;
-                T h = h_prev;
-                if (row_ok && jj >= 0 && jj < width) {
-                    const int j = j0 + jj;
-                    T d;
-                    if (kFused) {
-                        d = in_band(i, j, a.bw) ? load_cost<T, true>(a, b, s, t, i, j) : T(0);
-                    } else {
-                        const int kk = 32 * c + q;
-                        d = ring[((kk >> 5) % 3) * 1024 + (kk & 31) * 32 + t];
-                    }
-                    const Cell<T> cc = dp_cell<T, true>(i, j, a.bw, d, u, l_carry, a.k, a.gln2);
-                    pd_s[jj * 32 + t] = cc.pd;
-                    pu_s[jj * 32 + t] = cc.pu;
-                    pl_s[jj * 32 + t] = cc.pl;
-                    l_carry = cc.v;
-                    h = cc.h;
-                }
-                h_prev = h;
-            }
-            if (!polled && s < a.S - 1)
-                sbv = poll_entries<T>(A.sbt + ((size_t)b * a.S + (s + 1)) * a.M + (j0 - 1), width, epoch, t);
-            sio_s[t] = sbv;
-            __syncwarp();
-            // ---- phase E ----
-            T s_prev = T(0);
-            for (int q = 0; q < width + 31; ++q) {
-                const int jj = width - 1 - q + (31 - t);
-                const int jj31 = width - 1 - q;
-                const T src = (t == 0) ? sio_s[jj31 >= 0 ? jj31 : 0] : s_prev;
-                const T s_in = __shfl_sync(kFull, src, (t + 1) & 31);
-                T s_out = s_prev;
-                if (jj >= 0 && jj < width) {
-                    T e = T(0);
-                    if (row_ok) {
-                        const int j = j0 + jj;
-                        if (i == a.N && j == a.M) e = T(1);
-                        else if (!in_band(i, j, a.bw)) e = T(0);
-                        else {
-                            e = fma(e_right, pl_right, s_in);
-                            e = e < T(1) ? e : T(1);
-                        }
-                        const T pd = pd_s[jj * 32 + t], pu = pu_s[jj * 32 + t], pl = pl_s[jj * 32 + t];
-                        s_out = fma(e, pu, e_right * pd_right);
-                        e_right = e;
-                        pl_right = pl;
-                        pd_right = pd;
-                    }
-                    et_s[t * 32 + jj] = e;
-                    if (t == 0) halo_s[jj] = s_out;
-                }
-                s_prev = s_out;
-            }
-            __syncwarp();
-            // hand the top row's S to the strip above first (critical path)
-            if (t < width) TG::store(A.sbt + ((size_t)b * a.S + s) * a.M + (j0 - 1) + t, halo_s[t], epoch);
-            if (a.E) {
-                for (int r = 0; r < 32; ++r) {
-                    const int ir = 32 * s + r + 1;
-                    if (ir <= a.N && t < width)
-                        a.E[((size_t)b * a.N + (ir - 1)) * a.M + (j0 - 1) + t] = et_s[r * 32 + t];
-                }
-            }
-            // then queue the tile for the contraction kernel (or contract here)
-            unsigned slot = 0;
-            if (t == 0) {
-                atomicAdd(&A.stats[0], 1u);
-                slot = atomicAdd(&A.stats[1], 1u);
-            }
-            slot = __shfl_sync(kFull, slot, 0);
-            if (slot < A.tile_cap) {
-                T *dst = A.tiles + (size_t)slot * 1024;
-                for (int r = 0; r < 32; ++r) dst[r * 32 + t] = (t < width) ? et_s[r * 32 + t] : T(0);
-                if (t == 0) A.tile_meta[slot] = make_int4(b, s, c, width);
-            } else {
-                if (t == 0) atomicAdd(&A.stats[2], 1u);
-                tile_contract_fx<T>(A, fx, b, s, c, width, et_s, pd_s, t);
-            }
-            __syncwarp();
         }
     }
 }

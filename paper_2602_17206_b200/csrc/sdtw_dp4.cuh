@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
         const typename TG::Ent *sb_below = A.sbt + ((size_t)b * a.S + s + 1) * a.M;
         if (A.trace && t == 0) A.trace[2 * ((size_t)a.B * a.S + (size_t)b * a.S + s)] = global_ns();
         int ntiles = 0;
+        int nstored = 0;  // tiles of this strip in the store
         // cycle accounting (trace mode): [32 B S + 8 (b S + s) + e]: e = 0
         // recompute, 1 S wait, 2 E steps, 3 status waits, 4 tile epilogue, 5 other
         long long cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -564,14 +565,15 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                         a.E[((size_t)b * a.N + (ir - 1)) * a.M + (j0 - 1) + t] = et_s[r * 34 + t];
                 }
             }
-            // queue the tile for the contraction kernel (or contract here)
-            unsigned slot = 0;
-            if (t == 0) slot = atomicAdd(&A.stats[1], 1u);
-            slot = __shfl_sync(kFull, slot, 0);
-            if (slot < A.tile_cap) {
-                T *dst = A.tiles + (size_t)slot * 1024;
+            // queue the tile for the contraction (or contract here): the
+            // k-th stored tile of a strip is fixed by the strip's own order,
+            // so the split between the two paths is deterministic
+            if (nstored < A.tile_quota) {
+                const size_t slot = ((size_t)b * a.S + s) * A.tile_quota + nstored;
+                T *dst = A.tiles + slot * 1024;
                 for (int r = 0; r < 32; ++r) dst[r * 32 + t] = (t < width) ? et_s[r * 34 + t] : T(0);
                 if (t == 0) A.tile_meta[slot] = make_int4(b, s, c, width);
+                ++nstored;
             } else {
                 if (t == 0) atomicAdd(&A.stats[2], 1u);
                 // the speculative tile's probabilities live in the other slot;
@@ -587,6 +589,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             --c;
         }
         lap(5);
+        if (t == 0) A.strip_tiles[(size_t)b * a.S + s] = nstored;
         if (A.trace && t == 0)
             for (int e = 0; e < 8; ++e)
                 A.trace[32 * (size_t)a.B * a.S + 8 * ((size_t)b * a.S + s) + e] = (unsigned long long)cyc[e];

@@ -1,0 +1,228 @@
+// sdtw_grad.cuh — input gradients from the backward's non-zero E tiles,
+// deterministic and atomic-free.
+//
+// Reference: input_gradients (backward.hpp:208-266):
+//   dX_i = 2 (x_i sum_j E_ij - sum_j E_ij y_j),  dY_j = 2 (y_j sum_i E_ij - sum_i E_ij x_i).
+// The backward stores every non-zero 32 x 32 E tile of strip (b, s) in that
+// strip's slots of the tile store, in its own processing order, so the dX
+// bucket of a strip is simply its slot range; the dY buckets (per chunk)
+// come from a counting sort, each bucket sorted by strip.  One CTA per bucket
+// contracts its tiles in that fixed order (fp32 dot products, fp64
+// marginals): the result is bit-identical run to run (the reference's
+// determinism guarantee, acceptance.cpp:348-377) without atomics.  Tiles past
+// a strip's quota (only when the store is capped) were contracted by the
+// backward itself into 64-bit fixed-point accumulators (deterministic too)
+// and are added by finalize_grads_fx_add_kernel.
+#pragma once
+#include "sdtw_common.cuh"
+#include "sdtw_dp3.cuh"
+
+namespace sdtw {
+
+// Chunk buckets: count the stored tiles of each (b, c).
+__global__ void tile_hist_kernel(const int4 *__restrict__ meta, const int *__restrict__ strip_tiles, int quota,
+                                 int nstrips, int C, int *cnt_c)
+{
+    const size_t n = (size_t)nstrips * quota;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        if ((int)(i % quota) >= strip_tiles[i / quota]) continue;
+        const int4 m = meta[i];
+        atomicAdd(cnt_c + m.x * C + m.z, 1);
+    }
+}
+
+// Exclusive scan of cnt[0..n) into off[0..n] (one block).
+__global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int *__restrict__ cnt, int n, int *__restrict__ off)
+{
+    __shared__ int warp_sums[32];
+    __shared__ int carry;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + tid;
+        const int v = i < n ? cnt[i] : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int s = warp_sums[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        const int excl = carry + (w > 0 ? warp_sums[w - 1] : 0) + x - v;
+        if (i < n) off[i] = excl;
+        __syncthreads();
+        if (tid == 1023) carry = excl + v;
+        __syncthreads();
+    }
+    if (tid == 0) off[n] = carry;
+}
+
+// Bucket fill: cnt is consumed (counted down), so positions are unique;
+// the order inside a bucket is fixed afterwards by segment_sort_kernel.
+__global__ void tile_scatter_kernel(const int4 *__restrict__ meta, const int *__restrict__ strip_tiles, int quota,
+                                    int nstrips, int C, const int *__restrict__ off_c, int *cnt_c, int *ord_c)
+{
+    const size_t n = (size_t)nstrips * quota;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        if ((int)(i % quota) >= strip_tiles[i / quota]) continue;
+        const int4 m = meta[i];
+        const int kc = m.x * C + m.z;
+        ord_c[off_c[kc] + atomicSub(cnt_c + kc, 1) - 1] = (int)i;
+    }
+}
+
+// Insertion sort of each chunk bucket by strip (meta.y).
+__global__ void segment_sort_kernel(const int *__restrict__ off, int *ord, const int4 *__restrict__ meta, int nseg)
+{
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nseg; k += gridDim.x * blockDim.x) {
+        const int lo = off[k], hi = off[k + 1];
+        for (int a = lo + 1; a < hi; ++a) {
+            const int v = ord[a];
+            const int kv = meta[v].y;
+            int p = a - 1;
+            while (p >= lo && meta[ord[p]].y > kv) {
+                ord[p + 1] = ord[p];
+                --p;
+            }
+            ord[p + 1] = v;
+        }
+    }
+}
+
+// One CTA per bucket (strip b,s for which = 0; chunk b,c for which = 1):
+//   acc[o][k] = sum over the bucket's tiles (fixed order) of sum_m E_o,m p_m,k
+//   marg[o]   = sum over tiles of sum_m E_o,m
+//   grad[o][k] = 2 (v[o][k] marg[o] - acc[o][k])
+// o = output row (strip row / chunk column), m = partner index (chunk column /
+// strip row), p = partner rows (y chunk / x strip).  Buckets: which = 0: the
+// strip's own slots [key quota, + strip_tiles[key]); which = 1: ord[off[key]
+// .. off[key + 1]).  256 threads, each a 4 (o) x 4 (k) register block of a
+// 32 x 128 feature block: per partner index one 16-byte shared load of E and
+// one of p feed 16 FMAs.  Dot products accumulate in fp32 (fixed order), the
+// marginals and the final 2 (v marg - acc) in fp64.
+template <class T>
+__global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restrict__ tiles, const int4 *__restrict__ meta,
+                                                               const int *__restrict__ strip_tiles, int quota,
+                                                               const int *__restrict__ off, const int *__restrict__ ord,
+                                                               int which, int B, int S, int C, int N, int M, int D,
+                                                               const T *__restrict__ vout, const T *__restrict__ vpart,
+                                                               T *__restrict__ grad)
+{
+    __shared__ __align__(16) T Et[32][36];   // [m][o]
+    __shared__ __align__(16) T P[32][132];   // [m][k]
+    __shared__ double marg_s[32];
+    const int tid = threadIdx.x;
+    const int og = tid >> 5, kg = tid & 31;  // rows 4 og .. +3, features 4 kg .. +3
+    const int per_b = which == 0 ? S : C;
+    const int Rout = which == 0 ? N : M, Rpart = which == 0 ? M : N;
+    for (int key = blockIdx.x; key < B * per_b; key += gridDim.x) {
+        const int b = key / per_b, blk = key % per_b;
+        const int o0 = 32 * blk;
+        const int lo = which == 0 ? key * quota : off[key];
+        const int hi = which == 0 ? lo + strip_tiles[key] : off[key + 1];
+        const T *vo = vout + (size_t)b * Rout * D;
+        const T *vp = vpart + (size_t)b * Rpart * D;
+        T *g = grad + (size_t)b * Rout * D;
+        for (int kb = 0; kb < D; kb += 128) {
+            T acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[a][q] = T(0);
+            double marg[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int e = lo; e < hi; ++e) {
+                const int idx = which == 0 ? e : ord[e];
+                const int4 m = meta[idx];
+                const T *et = tiles + (size_t)idx * 1024;  // [r][jj]
+                const int p0 = which == 0 ? 32 * m.z : 32 * m.y;
+                const int np = which == 0 ? m.w : min(32, N - 32 * m.y);
+                __syncthreads();
+                for (int u = tid; u < 1024; u += 256) {
+                    const int r = u >> 5, jj = u & 31;
+                    const T v = et[u];
+                    if (which == 0) Et[jj][r] = v;  // o = r, m = jj
+                    else Et[r][jj] = v;             // o = jj, m = r
+                }
+                for (int u = tid; u < 32 * 128; u += 256) {
+                    const int r = u >> 7, k = u & 127;
+                    P[r][k] = (r < np && kb + k < D) ? vp[(size_t)(p0 + r) * D + kb + k] : T(0);
+                }
+                __syncthreads();
+                for (int mm = 0; mm < np; ++mm) {
+                    T ev[4], pv[4];
+                    if constexpr (sizeof(T) == 4) {
+                        const float4 e4 = *reinterpret_cast<const float4 *>(&Et[mm][4 * og]);
+                        const float4 p4 = *reinterpret_cast<const float4 *>(&P[mm][4 * kg]);
+                        ev[0] = e4.x; ev[1] = e4.y; ev[2] = e4.z; ev[3] = e4.w;
+                        pv[0] = p4.x; pv[1] = p4.y; pv[2] = p4.z; pv[3] = p4.w;
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) {
+                            ev[a] = Et[mm][4 * og + a];
+                            pv[a] = P[mm][4 * kg + a];
+                        }
+                    }
+                    if (kb == 0 && kg == 0) {
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) marg[a] += (double)ev[a];
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) acc[a][q] = fma(ev[a], pv[q], acc[a][q]);
+                }
+            }
+            if (kb == 0 && kg == 0) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a) marg_s[4 * og + a] = marg[a];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int o = 4 * og + a;
+                if (o0 + o >= Rout) continue;
+                const double mg = marg_s[o];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = kb + 4 * kg + q;
+                    if (k < D) {
+                        const size_t id = (size_t)(o0 + o) * D + k;
+                        g[id] = (T)(2.0 * ((double)vo[id] * mg - (double)acc[a][q]));
+                    }
+                }
+            }
+        }
+    }
+}
+
+// grad += 2 (v * marginal - acc) from the fixed-point accumulators (tiles the
+// capped store could not hold).
+template <class T>
+__global__ void finalize_grads_fx_add_kernel(const T *__restrict__ v, const long long *__restrict__ marg_fx,
+                                             const long long *__restrict__ acc_fx, const unsigned *absmax, int N,
+                                             int M, int rows, int D, int which, T *__restrict__ grad)
+{
+    const FxScales fx = fx_scales(absmax, N, M);
+    const double sm = 1.0 / (which == 0 ? fx.rs : fx.cs);
+    const double sa = 1.0 / (which == 0 ? fx.gx : fx.gy);
+    const size_t total = (size_t)rows * D;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = idx / D;
+        const double marg = (double)marg_fx[r] * sm;
+        const double acc = (double)acc_fx[idx] * sa;
+        if (marg != 0.0 || acc != 0.0) grad[idx] = (T)((double)grad[idx] + 2.0 * ((double)v[idx] * marg - acc));
+    }
+}
+
+}  // namespace sdtw

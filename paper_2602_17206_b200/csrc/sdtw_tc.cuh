@@ -164,6 +164,22 @@ __device__ __forceinline__ void split_store8(const float *src, float s, uint8_t 
     *reinterpret_cast<uint4 *>(lo + off) = *reinterpret_cast<const uint4 *>(l);
 }
 
+// split_store8 from registers (8 values already loaded).
+__device__ __forceinline__ void split_store8_regs(const float4 (&v)[2], float s, uint8_t *hi, uint8_t *lo, uint32_t off)
+{
+    const float f[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
+    __align__(16) __half h[8];
+    __align__(16) __half l[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float w = f[e] * s;
+        h[e] = __float2half_rn(w);
+        l[e] = __float2half_rn(w - __half2float(h[e]));
+    }
+    *reinterpret_cast<uint4 *>(hi + off) = *reinterpret_cast<const uint4 *>(h);
+    *reinterpret_cast<uint4 *>(lo + off) = *reinterpret_cast<const uint4 *>(l);
+}
+
 }  // namespace tc
 
 // max |v| over a float array -> atomicMax on the bit pattern (non-negative floats
@@ -249,16 +265,62 @@ __global__ void __launch_bounds__(128, 1)
     const int kchunks = (D + kCgK - 1) / kCgK;
     const bool vec = (D & 7) == 0;
     uint32_t phase = 0;
-    for (int kc = 0; kc < kchunks; ++kc) {
-        // stage X rows [i0, i0+128) and Y rows [j0, j0+128), features [64 kc, 64 kc + 64)
-        for (int u = tid; u < 128 * 8; u += 128) {
+    // Operand chunks (X rows [i0, i0+128), Y rows [j0, j0+128), features
+    // [64 kc, 64 kc + 64)) go through registers: the loads of chunk kc + 1 are
+    // in flight while the MMAs of chunk kc run.  Thread item i: row
+    // (tid + 128 i) >> 3, K block (tid + 128 i) & 7.
+    float4 px[8][2], py[8][2];
+    auto load_chunk = [&](int kc) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int u = tid + 128 * i;
             const int r = u >> 3, kb = u & 7;
             const int k = kc * kCgK + kb * 8;
-            const uint32_t off = tc::kmajor_off(r, kb, 2048);
             const int nk = max(0, min(8, D - k));
-            tc::split_store8(xb + (size_t)(i0 + r) * D + k, sc.sx, a_hi, a_lo, off, i0 + r < N ? nk : 0, vec);
-            tc::split_store8(yb + (size_t)(j0 + r) * D + k, sc.sy, b_hi, b_lo, off, j0 + r < M ? nk : 0, vec);
+            const int nx = i0 + r < N ? nk : 0, ny = j0 + r < M ? nk : 0;
+            const float *sx = xb + (size_t)min(i0 + r, N - 1) * D + min(k, D - 1);
+            const float *sy = yb + (size_t)min(j0 + r, M - 1) * D + min(k, D - 1);
+            if (vec && nx == 8) {
+                px[i][0] = __ldg(reinterpret_cast<const float4 *>(sx));
+                px[i][1] = __ldg(reinterpret_cast<const float4 *>(sx) + 1);
+            } else {
+                float f[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[e] = e < nx ? sx[e] : 0.f;
+                px[i][0] = make_float4(f[0], f[1], f[2], f[3]);
+                px[i][1] = make_float4(f[4], f[5], f[6], f[7]);
+            }
+            if (vec && ny == 8) {
+                py[i][0] = __ldg(reinterpret_cast<const float4 *>(sy));
+                py[i][1] = __ldg(reinterpret_cast<const float4 *>(sy) + 1);
+            } else {
+                float f[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[e] = e < ny ? sy[e] : 0.f;
+                py[i][0] = make_float4(f[0], f[1], f[2], f[3]);
+                py[i][1] = make_float4(f[4], f[5], f[6], f[7]);
+            }
         }
+    };
+    auto store_chunk = [&]() {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int u = tid + 128 * i;
+            const uint32_t off = tc::kmajor_off(u >> 3, u & 7, 2048);
+            tc::split_store8_regs(px[i], sc.sx, a_hi, a_lo, off);
+            tc::split_store8_regs(py[i], sc.sy, b_hi, b_lo, off);
+        }
+    };
+    load_chunk(0);
+    for (int kc = 0; kc < kchunks; ++kc) {
+        if (kc > 0) {
+            // the previous chunk's MMAs still read the operand tiles
+            tc::mbar_wait(&mma_bar, phase);
+            phase ^= 1u;
+            tc::tc_fence_after();
+        }
+        store_chunk();
+        if (kc + 1 < kchunks) load_chunk(kc + 1);
         tc::fence_async_smem();
         __syncthreads();
         if (tid == 0) {
@@ -275,10 +337,11 @@ __global__ void __launch_bounds__(128, 1)
             }
             tc::mma_commit(&mma_bar);
         }
-        tc::mbar_wait(&mma_bar, phase);
-        phase ^= 1u;
-        tc::tc_fence_after();
+        __syncwarp();
     }
+    tc::mbar_wait(&mma_bar, phase);
+    phase ^= 1u;
+    tc::tc_fence_after();
 
     // epilogue: warp w owns TMEM lanes 32w..32w+31 = rows i0 + 32w + lane
     float *stage = reinterpret_cast<float *>(smem) + warp * 32 * kCgStagePitch;  // [t][jj]

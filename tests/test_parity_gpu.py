@@ -260,3 +260,21 @@ def test_table_api_matches_reference(engine, golden):
         gx, gy = engine.input_gradients(c["E"], c["x"], c["y"])
         assert rel_err(gx, c["grad_x"]).max() <= 1e-12
         assert rel_err(gy, c["grad_y"]).max() <= 1e-12
+
+
+def test_tile_store_overflow_path(engine, oracle_c, monkeypatch):
+    """A tile quota of 1 per strip sends the other non-zero tiles
+    through the backward's in-warp fixed-point contraction; gradients still
+    match the fp64 oracle and are deterministic."""
+    x, y = _bench_like(2, 200, 24, seed=21)
+    _, rl, rgx, rgy = oracle_c.sdtw_with_gradients(x.astype(np.float64), y.astype(np.float64), 1.0)
+    ref = (rl, rgx, rgy)
+    monkeypatch.setenv("SDTW_DEBUG_TILE_QUOTA", "1")
+    a = engine.sdtw_with_gradients(x, y, 1.0)
+    b = engine.sdtw_with_gradients(x, y, 1.0)
+    monkeypatch.delenv("SDTW_DEBUG_TILE_QUOTA")
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+    assert rel_err(a[0], ref[0]).max() <= F32_LOSS
+    for g, r in zip(a[1:], ref[1:]):
+        assert grad_stats(g, r)[0] <= F32_GRAD_MAX
