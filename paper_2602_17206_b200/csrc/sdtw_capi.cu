@@ -398,16 +398,18 @@ struct Pipeline {
         Phase ph(ctx, 0);
         absmax = Buf<unsigned>(ctx, 2);
         CUDA_OK(cudaMemsetAsync(absmax.p, 0, 2 * sizeof(unsigned), ctx->stream));
-        LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * N * D, 256, 1024), 256, 0, x,
-               (size_t)B * N * D, absmax.p);
-        LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * M * D, 256, 1024), 256, 0, y,
-               (size_t)B * M * D, absmax.p + 1);
         xn = Buf<T>(ctx, (size_t)B * N);
         yn = Buf<T>(ctx, (size_t)B * M);
         if constexpr (std::is_same<T, float>::value) {
-            LAUNCH(ctx, sdtw::norms_f32_kernel, grid_for((size_t)B * N, 128), 128, 0, x, B * N, D, xn.p);
-            LAUNCH(ctx, sdtw::norms_f32_kernel, grid_for((size_t)B * M, 128), 128, 0, y, B * M, D, yn.p);
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)((B * N + 7) / 8), 256, 0, x, B * N, D, xn.p,
+                   absmax.p);
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)((B * M + 7) / 8), 256, 0, y, B * M, D, yn.p,
+                   absmax.p + 1);
         } else {
+            LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * N * D, 256, 1024), 256, 0, x,
+                   (size_t)B * N * D, absmax.p);
+            LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * M * D, 256, 1024), 256, 0, y,
+                   (size_t)B * M * D, absmax.p + 1);
             LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * N, 128), 128, 0, x, B * N, D, xn.p);
             LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * M, 128), 128, 0, y, B * M, D, yn.p);
         }
@@ -426,9 +428,17 @@ struct Pipeline {
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, sdtw::kCgSmem));
                 attr = true;
             }
-            dim3 grid((M + sdtw::kCgCols - 1) / sdtw::kCgCols, (N + sdtw::kCgRows - 1) / sdtw::kCgRows, B);
-            LAUNCH(ctx, sdtw::cost_gemm_tc_kernel, grid, 128, sdtw::kCgSmem, x, y, xn.p, yn.p, absmax.p, B,
-                   N, M, D, S, KK, bw, dsk.p);
+            // operands packed once (fp16 hi/lo core-matrix images), then
+            // bulk-copied by every CTA that needs them
+            const int NB = (N + 127) / 128;
+            Buf<uint8_t> xp(ctx, (size_t)B * NB * 128 * dpad * 4), yp(ctx, (size_t)B * C * 32 * dpad * 4);
+            LAUNCH(ctx, sdtw::pack_split_kernel, grid_for(xp.n / 64, 256, 8192), 256, 0, x, B, N, D, dpad, 128,
+                   absmax.p, 0, xp.p);
+            LAUNCH(ctx, sdtw::pack_split_kernel, grid_for(yp.n / 64, 256, 8192), 256, 0, y, B, M, D, dpad, 32,
+                   absmax.p, 1, yp.p);
+            dim3 grid((M + 127) / 128, NB, B);
+            LAUNCH(ctx, sdtw::cost_gemm_tc_kernel, grid, 256, sdtw::kCgSmem, xp.p, yp.p, xn.p, yn.p, absmax.p, B,
+                   N, M, S, C, KK, bw, dpad, dsk.p);
         } else {
             LAUNCH(ctx, sdtw::cost_skewed_kernel<T>, grid_for(total, 256), 256, 0, x, y, xn.p, yn.p, B,
                    N, M, D, S, KK, bw, dsk.p);
@@ -550,6 +560,11 @@ struct Pipeline {
                 const unsigned grid = (unsigned)std::max(1, std::min((work + 1) / 2, ctx->sm_count));
                 LAUNCH(ctx, sdtw::sdtw_forward_tc_kernel, grid, sdtw::kFtcThreads, smem, A, ftc());
             }
+        } else if (const char *e = std::getenv("SDTW_DEBUG_FWD_K")) {  // experiment hook
+            const int k = std::atoi(e);
+            if (k >= 4) launch_forward3<4>();
+            else if (k == 2) launch_forward3<2>();
+            else launch_forward3<1>();
         } else if (strips >= 4 * slots) launch_forward3<4>();
         else if (strips >= 2 * slots) launch_forward3<2>();
         else launch_forward3<1>();

@@ -212,48 +212,68 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                     }
                     xl = true;
                 }
-                for (int kh = 0; kh < dpad / 64; ++kh) {
-                    // y chunks cr - z, features [64 kh, 64 kh + 64): 32 rows x 64
+                // units u = (chunk z, K half kh): raw rows by cp.async one unit
+                // ahead, split into one of two stage buffers, MMAs per unit
+                // (the per-element instruction sequence is unchanged: for each
+                // chunk the K halves in order, 4 K steps of hi.hi, hi.lo,
+                // lo.hi each)
+                const int KH = dpad / 64, U = nt * KH;
+                const uint32_t xh = tc::smem_u32(xs), xlo = xh + 32u * dpad * 2;
+                auto unit_raw = [&](int u) {
+                    const int z = u / KH, kh = u % KH;
+                    raw_rows_async(raw + (u & 1) * 32 * 68, yg, a.D, 32 * (cr - z), 32, a.M, 64 * kh, 64, a.D, t);
+                    cp_async_commit();
+                };
+                bool pend[2] = {false, false};
+                if (async_ok) unit_raw(0);
+                for (int u = 0; u < U; ++u) {
+                    const int z = u / KH, kh = u % KH, sb = u & 1;
+                    uint8_t *st = stage + sb * 8192;
+                    if (pend[sb]) {  // the MMAs of unit u - 2 read this stage buffer
+                        tc::mbar_wait(&tc_bar[sb], tc_ph[sb]);
+                        tc_ph[sb] ^= 1u;
+                        pend[sb] = false;
+                        tc::tc_fence_after();
+                    }
                     if (async_ok) {
-                        for (int z = 0; z < nt; ++z)
-                            raw_rows_async(raw + z * 32 * 68, yg, a.D, 32 * (cr - z), 32, a.M, 64 * kh, 64, a.D, t);
-                        cp_async_commit();
-                        cp_async_wait<0>();
+                        if (u + 1 < U) {
+                            unit_raw(u + 1);
+                            cp_async_wait<1>();
+                        } else {
+                            cp_async_wait<0>();
+                        }
                         __syncwarp();
-                        for (int z = 0; z < nt; ++z)
-                            split_raw_rows(raw + z * 32 * 68, 32, 64, sc.sy, stage + z * 8192, stage + z * 8192 + 4096, 0,
-                                           512, t);
+                        split_raw_rows(raw + sb * 32 * 68, 32, 64, sc.sy, st, st + 4096, 0, 512, t);
                     } else {
-                        for (int z = 0; z < nt; ++z)
-                            stage_split_rows(yg + (size_t)64 * kh, a.D, 32 * (cr - z), 32, a.M, a.D - 64 * kh, 64, sc.sy,
-                                             stage + z * 8192, t);
+                        stage_split_rows(yg + (size_t)64 * kh, a.D, 32 * (cr - z), 32, a.M, a.D - 64 * kh, 64, sc.sy, st, t);
                     }
                     tc::fence_async_smem();
                     __syncwarp();
-                    lap(6);
                     tc::tc_fence_after();
                     if (t == 0) {
-                        const uint32_t xh = tc::smem_u32(xs), xlo = xh + 32u * dpad * 2;
-                        for (int z = 0; z < nt; ++z) {
-                            const uint32_t bh = tc::smem_u32(stage + z * 8192), bl = bh + 4096;
-                            for (int ks = 0; ks < 4; ++ks) {
-                                const int kg = 4 * kh + ks;
-                                const uint32_t oa = kg * 1024, ob = ks * 1024;
-                                const uint32_t acc0 = kg > 0 ? 1u : 0u;
-                                const uint32_t d = tmem + 32u * z;
-                                tc::mma_f16(d, tc::smem_desc(xh + oa, 512, 128), tc::smem_desc(bh + ob, 512, 128), idesc, acc0);
-                                tc::mma_f16(d, tc::smem_desc(xh + oa, 512, 128), tc::smem_desc(bl + ob, 512, 128), idesc, 1u);
-                                tc::mma_f16(d, tc::smem_desc(xlo + oa, 512, 128), tc::smem_desc(bh + ob, 512, 128), idesc, 1u);
-                            }
+                        const uint32_t bh = tc::smem_u32(st), bl = bh + 4096;
+                        const uint32_t d = tmem + 32u * z;
+                        for (int ks = 0; ks < 4; ++ks) {
+                            const int kg = 4 * kh + ks;
+                            const uint32_t oa = kg * 1024, ob = ks * 1024;
+                            const uint32_t acc0 = kg > 0 ? 1u : 0u;
+                            tc::mma_f16(d, tc::smem_desc(xh + oa, 512, 128), tc::smem_desc(bh + ob, 512, 128), idesc, acc0);
+                            tc::mma_f16(d, tc::smem_desc(xh + oa, 512, 128), tc::smem_desc(bl + ob, 512, 128), idesc, 1u);
+                            tc::mma_f16(d, tc::smem_desc(xlo + oa, 512, 128), tc::smem_desc(bh + ob, 512, 128), idesc, 1u);
                         }
-                        tc::mma_commit(&tc_bar[0]);
+                        tc::mma_commit(&tc_bar[sb]);
                     }
                     __syncwarp();
-                    tc::mbar_wait(&tc_bar[0], tc_ph[0]);
-                    tc_ph[0] ^= 1u;
-                    tc::tc_fence_after();
-                    lap(7);
+                    pend[sb] = true;
                 }
+                lap(6);
+                for (int sb = 0; sb < 2; ++sb)
+                    if (pend[sb]) {
+                        tc::mbar_wait(&tc_bar[sb], tc_ph[sb]);
+                        tc_ph[sb] ^= 1u;
+                    }
+                tc::tc_fence_after();
+                lap(7);
                 for (int z = 0; z < nt; ++z) {
                     float acc[32];
                     tc::tmem_ld32(tmem + 32u * z, acc);

@@ -34,27 +34,6 @@
 #include "sdtw_tc.cuh"
 
 namespace sdtw {
-namespace tc {
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-}  // namespace tc
 
 // Operand staging: rows [r0, r0 + rows) of a [R][D] fp32 series, split into
 // fp16 hi / lo (scale sc) as the SWIZZLE_NONE K-major image of a rows-row
@@ -143,14 +122,6 @@ __device__ __forceinline__ void split_raw_rows(const float *raw, int rows, int k
     }
 }
 
-// The cost epilogue shared by all tensor-core paths (cost_gemm_tc_kernel's):
-// row i, column j (0-based), accumulator acc.
-__device__ __forceinline__ float tc_cost(float acc, float xi, float yj, float m2, bool ok)
-{
-    float v = fmaf(m2, acc, xi + yj);
-    v = v < 0.f ? 0.f : v;
-    return ok ? v : 0.f;
-}
 
 struct FusedTcArgs {
     int dpad;  // D rounded up to 64 (<= kFtcMaxD): the unfused GEMM's K padding

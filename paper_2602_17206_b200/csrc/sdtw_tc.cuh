@@ -109,6 +109,25 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar)
                  : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // 32 lanes x 32 consecutive fp32 columns: thread t gets lane (base+t), columns
 // [col, col+32).  The warp must own the lane quarter (warp_id % 4).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
@@ -182,17 +201,6 @@ __device__ __forceinline__ void split_store8_regs(const float4 (&v)[2], float s,
 
 }  // namespace tc
 
-// max |v| over a float array -> atomicMax on the bit pattern (non-negative floats
-// order like their bits).
-__global__ void absmax_kernel(const float *__restrict__ v, size_t n, unsigned *out)
-{
-    float m = 0.f;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        m = fmaxf(m, fabsf(v[i]));
-    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, off));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
-}
-
 // Power-of-two operand scales: |x * sx| <= 2^14, and 1/(sx sy).
 struct SplitScale {
     float sx, sy, inv;
@@ -211,48 +219,121 @@ __device__ __forceinline__ SplitScale split_scale(const unsigned *absmax)
     return s;
 }
 
-// Norms in double, rounded once (the cost epilogue's largest terms).
-__global__ void norms_f32_kernel(const float *__restrict__ x, int rows, int D, float *__restrict__ out)
+// Norms in double, rounded once (the cost epilogue's largest terms), and the
+// operand-scale maximum max|v| in the same pass: one warp per row, a fixed
+// butterfly reduction (deterministic).
+__global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__restrict__ x, int rows, int D,
+                                                               float *__restrict__ out, unsigned *absmax)
 {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    const float *e = x + (size_t)r * D;
-    double s = 0.0;
-    for (int k = 0; k < D; ++k) s = fma((double)e[k], (double)e[k], s);
-    out[r] = (float)s;
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    float mx = 0.f;
+    if (r < rows) {
+        const float *e = x + (size_t)r * D;
+        double s = 0.0;
+        if ((D & 3) == 0) {
+            for (int k = 4 * lane; k < D; k += 128) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(e + k));
+                s = fma((double)v.x, (double)v.x, s);
+                s = fma((double)v.y, (double)v.y, s);
+                s = fma((double)v.z, (double)v.z, s);
+                s = fma((double)v.w, (double)v.w, s);
+                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+            }
+        } else {
+            for (int k = lane; k < D; k += 32) {
+                const float v = e[k];
+                s = fma((double)v, (double)v, s);
+                mx = fmaxf(mx, fabsf(v));
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+        if (lane == 0) out[r] = (float)s;
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    if (lane == 0 && mx > 0.f) atomicMax(absmax, __float_as_uint(mx));
+}
+
+
+// The cost epilogue shared by all tensor-core paths (the unfused GEMM, the
+// fused forward and the fused backward recompute): accumulator acc of row i,
+// column j; d = ||x_i||^2 + ||y_j||^2 - 2 <x_i, y_j>, clamped at 0
+// (cost.hpp:63-78); 0 outside the matrix / band.
+__device__ __forceinline__ float tc_cost(float acc, float xi, float yj, float m2, bool ok)
+{
+    float v = fmaf(m2, acc, xi + yj);
+    v = v < 0.f ? 0.f : v;
+    return ok ? v : 0.f;
 }
 
 // ----------------------------------------------------------------------------
-// Unfused cost tensor on tcgen05: one CTA per (pair, 128-row block, 128-column
-// block).  Output in the DP's skewed strip layout dsk[b][s][kk][t] =
-// d(32 s + t + 1, kk - t + 1) (0-based kk row of KK = row_pitch rows), so
-// that every DP warp step reads one 128-byte line.  The epilogue stages the
-// 32 x 128 block of each warp in shared memory and writes whole skewed rows
-// (rows shared with a neighbouring CTA are lane-masked).
+// Operand packing for the unfused GEMM: rows [B][R][D] fp32 -> blocks
+// [B][nblk][hi|lo][dpad/8][rpb][8] fp16, the SWIZZLE_NONE K-major image of an
+// rpb-row operand tile (K-block stride rpb * 16 bytes); rows >= R and
+// features >= D zero.  One thread per 16-byte core-matrix row, split exactly
+// as split_store8.  which = 0: x (scale sx), 1: y (scale sy).
 // ----------------------------------------------------------------------------
-constexpr int kCgRows = 128, kCgCols = 128, kCgK = 64;
-constexpr int kCgTile = kCgRows * kCgK * 2;  // bytes of one fp16 operand tile (16 KB)
-constexpr int kCgStagePitch = kCgCols + 2;  // floats; odd bank step for skewed reads (2-way on writes)
-constexpr int kCgSmem = 4 * 32 * kCgStagePitch * 4;  // >= 4 operand tiles (64 KB); reused by the staging
+__global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, int D, int dpad, int rpb,
+                                  const unsigned *absmax, int which, uint8_t *__restrict__ dst)
+{
+    const int nblk = (R + rpb - 1) / rpb;
+    const int kbn = dpad / 8;
+    const size_t total = (size_t)B * nblk * rpb * kbn;
+    const SplitScale sc = split_scale(absmax);
+    const float s = which == 0 ? sc.sx : sc.sy;
+    const bool vec = (D & 7) == 0;
+    for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(u % rpb);        // row within the block (fastest: coalesced stores)
+        const size_t rest = u / rpb;
+        const int kb = (int)(rest % kbn);
+        const size_t bb = rest / kbn;        // b * nblk + blk
+        const int blk = (int)(bb % nblk);
+        const int b = (int)(bb / nblk);
+        const int row = blk * rpb + r;
+        uint8_t *hi = dst + bb * (size_t)rpb * dpad * 4;
+        uint8_t *lo = hi + (size_t)rpb * dpad * 2;
+        const int k = kb * 8;
+        const int nk = row < R ? max(0, min(8, D - k)) : 0;
+        const float *p = src + ((size_t)b * R + min(row, R - 1)) * D + min(k, D - 1);
+        tc::split_store8(p, s, hi, lo, tc::kmajor_off(r, kb, rpb * 16), nk, vec && nk == 8);
+    }
+}
 
-__global__ void __launch_bounds__(128, 1)
-    cost_gemm_tc_kernel(const float *__restrict__ x, const float *__restrict__ y,
-                        const float *__restrict__ xn, const float *__restrict__ yn, const unsigned *absmax,
-                        int B, int N, int M, int D, int S, int KK, int bw, float *__restrict__ dsk)
+// ----------------------------------------------------------------------------
+// Unfused cost tensor on tcgen05 (materialize_costs, cost.hpp:82-99): one CTA
+// per (pair, 128-row block, 128-column block).  Operands come from the packed
+// fp16 hi/lo images by bulk copies (TMA engine), 64 features per round: A =
+// the 128 x rows, B = five 32-column y chunks [j0 - 32, j0 + 128) (N = 32
+// MMAs into TMEM columns 32 z).  The extra chunk on the left lets the CTA
+// write whole rows of the DP's skewed strip layout
+//   dsk[b][s][kk][t] = d(32 s + t, kk - t)   (0-based, kk in [0, KK))
+// for kk in [j0, j0 + 128) with no row shared between CTAs: the epilogue
+// stages each warp's 32 x 160 block in shared memory (pitch 162: the skewed
+// reads are bank-conflict free) and writes four skewed rows (512 contiguous
+// bytes) per 16-byte store.  The last column block also writes the tail rows
+// up to KK.
+// ----------------------------------------------------------------------------
+constexpr int kCgPitch = 162;
+constexpr int kCgSmem = 4 * 32 * kCgPitch * 4;  // 82944 B >= one round's operands (72 KB)
+
+__global__ void __launch_bounds__(256, 1)
+    cost_gemm_tc_kernel(const uint8_t *__restrict__ xp, const uint8_t *__restrict__ yp, const float *__restrict__ xn,
+                        const float *__restrict__ yn, const unsigned *absmax, int B, int N, int M, int S, int C,
+                        int KK, int bw, int dpad, float *__restrict__ dsk)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *a_hi = smem, *a_lo = smem + kCgTile, *b_hi = smem + 2 * kCgTile, *b_lo = smem + 3 * kCgTile;
-    __shared__ uint64_t mma_bar;
+    __shared__ uint64_t bars[2];  // [0] operand bytes landed, [1] MMAs done
     __shared__ uint32_t tmem_base;
-
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int b = blockIdx.z;
-    const int i0 = blockIdx.y * kCgRows, j0 = blockIdx.x * kCgCols;
+    const int b = blockIdx.z, ib = blockIdx.y, jb = blockIdx.x;
+    const int i0 = 128 * ib, j0 = 128 * jb;
+    const int NB = (N + 127) / 128;
     const SplitScale sc = split_scale(absmax);
 
-    if (warp == 0) tc::tmem_alloc<128>(&tmem_base);
+    if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
     if (tid == 0) {
-        tc::mbar_init(&mma_bar, 1);
+        tc::mbar_init(&bars[0], 1);
+        tc::mbar_init(&bars[1], 1);
         tc::fence_barrier_init();
     }
     tc::tc_fence_before();
@@ -260,124 +341,121 @@ __global__ void __launch_bounds__(128, 1)
     tc::tc_fence_after();
     const uint32_t tmem = tmem_base;
 
-    const float *xb = x + (size_t)b * N * D, *yb = y + (size_t)b * M * D;
-    const uint32_t idesc = tc::idesc_f16_f32(128, kCgCols);
-    const int kchunks = (D + kCgK - 1) / kCgK;
-    const bool vec = (D & 7) == 0;
-    uint32_t phase = 0;
-    // Operand chunks (X rows [i0, i0+128), Y rows [j0, j0+128), features
-    // [64 kc, 64 kc + 64)) go through registers: the loads of chunk kc + 1 are
-    // in flight while the MMAs of chunk kc run.  Thread item i: row
-    // (tid + 128 i) >> 3, K block (tid + 128 i) & 7.
-    float4 px[8][2], py[8][2];
-    auto load_chunk = [&](int kc) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int u = tid + 128 * i;
-            const int r = u >> 3, kb = u & 7;
-            const int k = kc * kCgK + kb * 8;
-            const int nk = max(0, min(8, D - k));
-            const int nx = i0 + r < N ? nk : 0, ny = j0 + r < M ? nk : 0;
-            const float *sx = xb + (size_t)min(i0 + r, N - 1) * D + min(k, D - 1);
-            const float *sy = yb + (size_t)min(j0 + r, M - 1) * D + min(k, D - 1);
-            if (vec && nx == 8) {
-                px[i][0] = __ldg(reinterpret_cast<const float4 *>(sx));
-                px[i][1] = __ldg(reinterpret_cast<const float4 *>(sx) + 1);
-            } else {
-                float f[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) f[e] = e < nx ? sx[e] : 0.f;
-                px[i][0] = make_float4(f[0], f[1], f[2], f[3]);
-                px[i][1] = make_float4(f[4], f[5], f[6], f[7]);
-            }
-            if (vec && ny == 8) {
-                py[i][0] = __ldg(reinterpret_cast<const float4 *>(sy));
-                py[i][1] = __ldg(reinterpret_cast<const float4 *>(sy) + 1);
-            } else {
-                float f[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) f[e] = e < ny ? sy[e] : 0.f;
-                py[i][0] = make_float4(f[0], f[1], f[2], f[3]);
-                py[i][1] = make_float4(f[4], f[5], f[6], f[7]);
+    const uint8_t *xa = xp + ((size_t)b * NB + ib) * (size_t)128 * dpad * 4;
+    const uint32_t idesc = tc::idesc_f16_f32(128, 32);
+    const int rounds = dpad / 64;
+    int zlo = 0;
+    while (4 * jb - 1 + zlo < 0) ++zlo;  // chunk -1 does not exist
+    int zhi = 5;
+    while (zhi > zlo && 4 * jb - 1 + zhi - 1 >= C) --zhi;
+    for (int kc = 0; kc < rounds; ++kc) {
+        if (tid == 0) {
+            const uint32_t bytes = 32768u + (uint32_t)(zhi - zlo) * 8192u;
+            tc::mbar_expect_tx(&bars[0], bytes);
+            tc::bulk_g2s(smem, xa + (size_t)kc * 16384, 16384, &bars[0]);
+            tc::bulk_g2s(smem + 16384, xa + (size_t)128 * dpad * 2 + (size_t)kc * 16384, 16384, &bars[0]);
+            for (int z = zlo; z < zhi; ++z) {
+                const uint8_t *yb = yp + ((size_t)b * C + (4 * jb - 1 + z)) * (size_t)32 * dpad * 4;
+                tc::bulk_g2s(smem + 32768 + z * 8192, yb + (size_t)kc * 4096, 4096, &bars[0]);
+                tc::bulk_g2s(smem + 32768 + z * 8192 + 4096, yb + (size_t)32 * dpad * 2 + (size_t)kc * 4096, 4096,
+                             &bars[0]);
             }
         }
-    };
-    auto store_chunk = [&]() {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int u = tid + 128 * i;
-            const uint32_t off = tc::kmajor_off(u >> 3, u & 7, 2048);
-            tc::split_store8_regs(px[i], sc.sx, a_hi, a_lo, off);
-            tc::split_store8_regs(py[i], sc.sy, b_hi, b_lo, off);
-        }
-    };
-    load_chunk(0);
-    for (int kc = 0; kc < kchunks; ++kc) {
-        if (kc > 0) {
-            // the previous chunk's MMAs still read the operand tiles
-            tc::mbar_wait(&mma_bar, phase);
-            phase ^= 1u;
-            tc::tc_fence_after();
-        }
-        store_chunk();
-        if (kc + 1 < kchunks) load_chunk(kc + 1);
-        tc::fence_async_smem();
-        __syncthreads();
+        tc::mbar_wait(&bars[0], kc & 1);
         if (tid == 0) {
             tc::tc_fence_after();
-            const uint32_t ah = tc::smem_u32(a_hi), al = tc::smem_u32(a_lo);
-            const uint32_t bh = tc::smem_u32(b_hi), bl = tc::smem_u32(b_lo);
-#pragma unroll
-            for (int ks = 0; ks < kCgK / 16; ++ks) {
-                const uint32_t o = ks * 2 * 2048;
-                const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-                tc::mma_f16(tmem, tc::smem_desc(ah + o, 2048, 128), tc::smem_desc(bh + o, 2048, 128), idesc, acc0);
-                tc::mma_f16(tmem, tc::smem_desc(ah + o, 2048, 128), tc::smem_desc(bl + o, 2048, 128), idesc, 1u);
-                tc::mma_f16(tmem, tc::smem_desc(al + o, 2048, 128), tc::smem_desc(bh + o, 2048, 128), idesc, 1u);
+            const uint32_t ah = tc::smem_u32(smem), al = ah + 16384;
+            for (int z = zlo; z < zhi; ++z) {
+                const uint32_t bh = tc::smem_u32(smem + 32768 + z * 8192), bl = bh + 4096;
+                const uint32_t d = tmem + 32u * z;
+                for (int ks = 0; ks < 4; ++ks) {
+                    const int kg = 4 * kc + ks;
+                    const uint32_t oa = ks * 4096, ob = ks * 1024;
+                    const uint32_t acc0 = kg > 0 ? 1u : 0u;
+                    tc::mma_f16(d, tc::smem_desc(ah + oa, 2048, 128), tc::smem_desc(bh + ob, 512, 128), idesc, acc0);
+                    tc::mma_f16(d, tc::smem_desc(ah + oa, 2048, 128), tc::smem_desc(bl + ob, 512, 128), idesc, 1u);
+                    tc::mma_f16(d, tc::smem_desc(al + oa, 2048, 128), tc::smem_desc(bh + ob, 512, 128), idesc, 1u);
+                }
             }
-            tc::mma_commit(&mma_bar);
+            tc::mma_commit(&bars[1]);
         }
         __syncwarp();
+        tc::mbar_wait(&bars[1], kc & 1);  // the next round overwrites the operands
+        tc::tc_fence_after();
     }
-    tc::mbar_wait(&mma_bar, phase);
-    phase ^= 1u;
-    tc::tc_fence_after();
 
-    // epilogue: warp w owns TMEM lanes 32w..32w+31 = rows i0 + 32w + lane
-    float *stage = reinterpret_cast<float *>(smem) + warp * 32 * kCgStagePitch;  // [t][jj]
-    const int i = i0 + 32 * warp + lane;  // 0-based row
+    // epilogue: warp w reads TMEM lane quarter q = w & 3 (rows i0 + 32 q +
+    // lane); warps 0-3 take chunks z = 0..2, warps 4-7 chunks 3..4
+    const int q = warp & 3, hf = warp >> 2;
+    float *stage = reinterpret_cast<float *>(smem) + q * 32 * kCgPitch;
+    const int i = i0 + 32 * q + lane;
     const bool row_ok = i < N;
     const float xi = row_ok ? xn[(size_t)b * N + i] : 0.f;
     const float m2 = -2.0f * sc.inv;
-#pragma unroll 1
-    for (int cc = 0; cc < kCgCols / 32; ++cc) {
-        float acc[32];
-        tc::tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(32 * cc), acc);
+    const int zb = hf == 0 ? 0 : 3, ze = hf == 0 ? 3 : 5;
+    float yv[3];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-            const int j = j0 + 32 * cc + e;
-            float v = 0.f;
-            if (row_ok && j < M && in_band(i + 1, j + 1, bw)) {
-                v = fmaf(m2, acc[e], xi + yn[(size_t)b * M + j]);
-                v = v < 0.f ? 0.f : v;
+    for (int u = 0; u < 3; ++u) {
+        const int j = j0 - 32 + 32 * (zb + u) + lane;
+        yv[u] = (zb + u < ze && j >= 0 && j < M) ? yn[(size_t)b * M + j] : 0.f;
+    }
+    __syncthreads();  // all MMAs done and read: the operand area becomes the stage
+    // interior block: every column in [0, M), no band, all rows valid
+    const bool interior = j0 >= 32 && j0 + 128 <= M && bw == 0 && i0 + 128 <= N;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        const int z = zb + u;
+        if (z >= ze) break;
+        float acc[32];
+        if (z >= zlo && z < zhi) {
+            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * z), acc);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+        }
+        const int jz = j0 - 32 + 32 * z;
+        float *st = stage + lane * kCgPitch + 32 * z;
+        if (interior) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) st[e] = tc_cost(acc[e], xi, __shfl_sync(kFull, yv[u], e), m2, true);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+                const float yj = __shfl_sync(kFull, yv[u], e);
+                const int j = jz + e;
+                const bool ok = row_ok && j >= 0 && j < M && in_band(i + 1, j + 1, bw);
+                st[e] = tc_cost(acc[e], xi, yj, m2, ok);
             }
-            stage[lane * kCgStagePitch + 32 * cc + e] = v;
         }
     }
-    __syncwarp();
-    const int s = (i0 >> 5) + warp;
+    __syncthreads();
+    const int s = 4 * ib + q;
     if (32 * s < N) {
         float *ds = dsk + ((size_t)b * S + s) * (size_t)KK * 32;
-        // skewed rows kk = j + t over this block's columns j in [j0, j0 + 128)
-        const int kk_lo = j0, kk_hi = min(j0 + kCgCols, M) - 1 + 31;
-        for (int kk = kk_lo; kk <= kk_hi; ++kk) {
-            const int jl = kk - lane - j0;  // local column of this lane
-            if (jl >= 0 && jl < kCgCols && j0 + jl < M) ds[(size_t)kk * 32 + lane] = stage[lane * kCgStagePitch + jl];
+        const bool last = jb == (M + 127) / 128 - 1;
+        const int rend = last ? KK : min(j0 + 128, KK);
+        const int t4 = 4 * (lane & 7);
+        // the two warps of a lane quarter take alternate groups of 4 rows
+        for (int kk0 = j0 + 4 * hf; kk0 < rend; kk0 += 8) {
+            const int kk = kk0 + (lane >> 3);
+            const float *sr = stage + kk - j0 + 32;  // + t * (pitch - 1) - ... below
+            float v[4];
+            if (!last) {
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) v[c4] = sr[(t4 + c4) * (kCgPitch - 1)];
+            } else {
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    const int lc = kk - (t4 + c4) - j0 + 32;  // local column of lane t4 + c4
+                    v[c4] = lc < 160 ? stage[(t4 + c4) * kCgPitch + lc] : 0.f;
+                }
+            }
+            *reinterpret_cast<float4 *>(ds + (size_t)kk * 32 + t4) = make_float4(v[0], v[1], v[2], v[3]);
         }
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<128>(tmem);
+    if (warp == 0) tc::tmem_dealloc<256>(tmem);
 }
 
 }  // namespace sdtw
