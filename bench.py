@@ -7,9 +7,12 @@ step = loss + grad_x + grad_y of the whole batch (sdtw_with_gradients,
 backward.hpp:276-304).
 
 Default workload = BASELINE.json configs[1]: B=32, N=M=1024, D=128,
-gamma=0.1, FUSED (the headline `value`), with the UNFUSED mode of the same
-config measured in the same run (`unfused`).  `--config c3` runs the
-north-star case (L=4096, gamma=0.01).
+gamma=0.1, UNFUSED (the headline `value`), with the FUSED mode of the same
+config measured in the same run (`fused`).  `--config c3` runs the
+north-star case (L=4096, gamma=0.01; use --mode fused for its fused target),
+`--config c5` the Soft-DTW barycenter (B=1024 members, L=512, D=64): one
+step = objective + gradient over all members + NCCL allreduce of grad_z
+across ranks + Adam update (members sharded over ranks: strong scaling).
 
 Arms:
   (default)         this engine (libsdtw_b200.so through the C-ABI).
@@ -39,6 +42,7 @@ CONFIGS = {
     "c2": dict(B=32, L=1024, D=128, gamma=0.1),
     "c3": dict(B=32, L=4096, D=128, gamma=0.01),
     "c4": dict(B=32, L=256, D=1024, gamma=1.0),
+    "c5": dict(B=1024, L=512, D=64, gamma=1.0),
 }
 METRIC = "DP cells/sec (fwd+bwd, fused & unfused) at B=32 vs L,D; peak HBM MB; 1/2/4/8 GPU"
 SM_COUNT = 148
@@ -57,62 +61,93 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    polled every 2 ms in a thread (nvidia-smi's 100 ms floor would miss a
+    ~15 ms region); falls back to nvidia-smi -lms 100."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device: int):
         self.device = device
+        self.samples = []
+        self.reasons = set()
+        self.stop_flag = threading.Event()
+        self.thread = None
+        self.smax = None
         self.proc = None
         self.lines = []
-        self.thread = None
 
     def start(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                idx = int(vis.split(",")[self.device])
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self.stop_flag.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for nm, bit in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(nm)
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            pass
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
         except Exception:
             self.proc = None
-            return
-        self.thread = threading.Thread(target=self._read, daemon=True)
-        self.thread.start()
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        self.stop_flag.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for ln in self.lines:
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    self.samples.append(float(parts[0]))
+                    self.smax = max(self.smax or 0.0, float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[2:6]):
+                    if v.lower() == "active":
+                        self.reasons.add(nm)
         if self.thread:
             self.thread.join(timeout=2)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        sm = sorted(self.samples)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.smax,
+                "samples": len(sm), "reasons": sorted(self.reasons)}
 
 
 def _dist():
@@ -151,6 +186,8 @@ def run_reference_arm(args, cfg):
     ws, rank, _ = _dist()
     if rank != 0:
         return
+    if args.config == "c5":
+        return run_reference_barycenter(args, cfg, ws)
     threads = os.cpu_count() or 1
     fused = args.mode == "fused"
     pairs = _ref_pairs_for(cfg)
@@ -177,7 +214,173 @@ def run_reference_arm(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def _bary_inputs(cfg, np):
+    """C5 synthetic members (N(0,1), seeded) and the initial barycenter
+    (member 0), identical on every rank."""
+    rng = np.random.default_rng(42)
+    K, L, D = cfg["B"], cfg["L"], cfg["D"]
+    members = rng.standard_normal((K, L, D), dtype=np.float32)
+    return members, members[0].copy()
+
+
+def run_reference_barycenter(args, cfg, ws):
+    """The reference's barycenter_objective (barycenter.hpp:60-86, members
+    sequential, each sdtw_with_gradients on all host threads) on a bounded
+    member sample; Adam on the host."""
+    import numpy as np
+    import oracle
+    ref = oracle.Reference()
+    threads = os.cpu_count() or 1
+    members, z = _bary_inputs(cfg, np)
+    kp = 8  # members per reference step (the sample)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        rc, val, grad = ref.barycenter_objective(z, members[:kp], cfg["gamma"], threads=threads,
+                                                 dtype=np.float32)
+        times.append(time.perf_counter() - t0)
+        if rc != 0:
+            raise RuntimeError(f"reference barycenter_objective rc={rc}")
+    ms = 1e3 * sum(times[args.warmup:]) / args.steps
+    cells = kp * cfg["L"] * cfg["L"]
+    val = cells / (ms / 1e3)
+    sample = (f"reference barycenter_objective fp32 unfused log, {kp} of {cfg['B']} members, "
+              f"L={cfg['L']} D={cfg['D']} gamma={cfg['gamma']}, threads={threads}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "cells/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) members (numpy seed 42)", "config": _config_dict(args, cfg, ws),
+        "cpu_baseline": {"value": val, "unit": "cells/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_barycenter_arm(args, cfg):
+    """C5: Soft-DTW barycenter step on N GPUs (members sharded, strong
+    scaling), grad_z summed by the engine's NCCL allreduce."""
+    import numpy as np
+    import torch
+    from paper_2602_17206_b200 import Engine
+    from paper_2602_17206_b200.build import build
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        build()
+    if ws > 1:
+        dist.barrier()
+    eng = Engine(local)
+    side = torch.cuda.Stream()
+    torch.cuda.set_stream(side)
+    eng.set_stream(side.cuda_stream)
+    if ws > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(eng.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        eng.nccl_init(bytes(uid.cpu().numpy().tobytes()), ws, rank)
+    K, L, D, gamma = cfg["B"], cfg["L"], cfg["D"], cfg["gamma"]
+    members_h, z_h = _bary_inputs(cfg, np)
+    from paper_2602_17206_b200.sharding import shard_range
+    k0, k1 = shard_range(K, ws, rank)
+    mem = torch.from_numpy(members_h[k0:k1]).cuda()
+    z = torch.from_numpy(z_h).cuda()
+    g = torch.empty_like(z)
+    v = torch.zeros(1, dtype=torch.float64, device="cuda")
+    m1 = torch.zeros(z.numel(), dtype=torch.float64, device="cuda")
+    m2 = torch.zeros_like(m1)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(t):
+        eng.barycenter_objective(z, mem, gamma, grad_out=g, value_out=v)
+        if ws > 1:
+            eng.allreduce_grad(g, v)
+        eng.adam_step(z, g, m1, m2, t)
+
+    t = 0
+    for _ in range(args.warmup):
+        t += 1
+        step(t)
+    torch.cuda.synchronize()
+    eng.reset_launches()
+    eng.reset_peak()
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    total = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record(stream)
+        t += 1
+        step(t)
+        e_.record(stream)
+        e_.synchronize()
+        total += s_.elapsed_time(e_)
+    launches = eng.launches
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    tt = torch.tensor([total], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    max_ms = float(tt.item())
+    cells = K * L * L  # whole job per step
+    value = cells * args.steps / (max_ms / 1e3)
+    # e2e: host members and host z through the public API each step
+    mh = torch.from_numpy(members_h[k0:k1]).pin_memory()
+    zh = torch.from_numpy(z_h).pin_memory()
+    gh = torch.empty_like(zh).pin_memory()
+    e2e = 0.0
+    for _ in range(args.steps):
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record(stream)
+        eng.barycenter_objective(zh, mh, gamma, grad_out=gh)
+        e_.record(stream)
+        e_.synchronize()
+        e2e += s_.elapsed_time(e_)
+    te = torch.tensor([e2e], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic N(0,1) members (numpy seed 42)",
+            "config": _config_dict(args, cfg, ws),
+            "peak_hbm_mb": eng.mem_stats()[1] / 2**20,
+            "e2e": {"value": cells * args.steps / (float(te.item()) / 1e3), "unit": "cells/s",
+                    "h2d_bytes_per_step": int((k1 - k0) * L * D * 4 + L * D * 4),
+                    "d2h_bytes_per_step": int(L * D * 4 + 8),
+                    "note": "objective+gradient only (no allreduce/Adam), host members per call"},
+            "gpu_launches": launches, "roofline": None, "clocks": clk,
+            "collective": "NCCL allreduce of grad_z (+ objective) per step" if ws > 1 else None,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
 def _config_dict(args, cfg, ws):
+    if args.config == "c5":
+        return {"workload": f"c5: Soft-DTW barycenter, {cfg['B']} members L={cfg['L']} D={cfg['D']} "
+                            f"gamma={cfg['gamma']} unfused log, objective+grad+allreduce+Adam",
+                "members": cfg["B"], "global_batch": cfg["B"], "N": cfg["L"], "M": cfg["L"],
+                "D": cfg["D"], "gamma": cfg["gamma"], "cost_mode": "unfused",
+                "parallelism": f"dp{ws} (members sharded, NCCL allreduce of grad_z)",
+                "l2": "flushed between timed steps (256 MiB write)"}
     return {"workload": f"{args.config}: B={cfg['B']} N=M={cfg['L']} D={cfg['D']} "
                         f"gamma={cfg['gamma']} {args.mode} fwd+bwd (loss, grad_x, grad_y)",
             "B_per_gpu": cfg["B"], "global_batch": cfg["B"] * ws, "N": cfg["L"], "M": cfg["L"],
@@ -400,6 +603,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
+    elif args.config == "c5":
+        run_barycenter_arm(args, cfg)
     else:
         run_engine_arm(args, cfg)
 

@@ -401,9 +401,9 @@ struct Pipeline {
         xn = Buf<T>(ctx, (size_t)B * N);
         yn = Buf<T>(ctx, (size_t)B * M);
         if constexpr (std::is_same<T, float>::value) {
-            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)((B * N + 7) / 8), 256, 0, x, B * N, D, xn.p,
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * N + 7) / 8), 256, 0, x, B * N, D, xn.p,
                    absmax.p);
-            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)((B * M + 7) / 8), 256, 0, y, B * M, D, yn.p,
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * M + 7) / 8), 256, 0, y, B * M, D, yn.p,
                    absmax.p + 1);
         } else {
             LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * N * D, 256, 1024), 256, 0, x,
@@ -657,10 +657,10 @@ struct Pipeline {
             if (need_fx) {
                 if (gx)
                     LAUNCH(ctx, sdtw::finalize_grads_fx_add_kernel<T>, grid_for((size_t)B * N * D, 256), 256, 0, x,
-                           rs_fx.p, gx_fx.p, absmax.p, N, M, B * N, D, 0, gx);
+                           rs_fx.p, gx_fx.p, absmax.p, stats.p, N, M, B * N, D, 0, gx);
                 if (gy)
                     LAUNCH(ctx, sdtw::finalize_grads_fx_add_kernel<T>, grid_for((size_t)B * M * D, 256), 256, 0, y,
-                           cs_fx.p, gy_fx.p, absmax.p, N, M, B * M, D, 1, gy);
+                           cs_fx.p, gy_fx.p, absmax.p, stats.p, N, M, B * M, D, 1, gy);
             }
         }
         // the cost tensor is dropped after the backward (backward.hpp:291)

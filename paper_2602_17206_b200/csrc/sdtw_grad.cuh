@@ -209,9 +209,11 @@ __global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restri
 // capped store could not hold).
 template <class T>
 __global__ void finalize_grads_fx_add_kernel(const T *__restrict__ v, const long long *__restrict__ marg_fx,
-                                             const long long *__restrict__ acc_fx, const unsigned *absmax, int N,
-                                             int M, int rows, int D, int which, T *__restrict__ grad)
+                                             const long long *__restrict__ acc_fx, const unsigned *absmax,
+                                             const unsigned *stats, int N, int M, int rows, int D, int which,
+                                             T *__restrict__ grad)
 {
+    if (stats[2] == 0) return;  // no tile overflowed the store: nothing to add
     const FxScales fx = fx_scales(absmax, N, M);
     const double sm = 1.0 / (which == 0 ? fx.rs : fx.cs);
     const double sa = 1.0 / (which == 0 ? fx.gx : fx.gy);

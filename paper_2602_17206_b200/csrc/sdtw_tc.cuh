@@ -225,10 +225,11 @@ __device__ __forceinline__ SplitScale split_scale(const unsigned *absmax)
 __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__restrict__ x, int rows, int D,
                                                                float *__restrict__ out, unsigned *absmax)
 {
-    const int lane = threadIdx.x & 31;
-    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    __shared__ float wmax[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     float mx = 0.f;
-    if (r < rows) {
+    // grid-stride over rows (one warp per row): one atomic per block at the end
+    for (int r = blockIdx.x * 8 + w; r < rows; r += gridDim.x * 8) {
         const float *e = x + (size_t)r * D;
         double s = 0.0;
         if ((D & 3) == 0) {
@@ -251,9 +252,14 @@ __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__re
         if (lane == 0) out[r] = (float)s;
     }
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-    if (lane == 0 && mx > 0.f) atomicMax(absmax, __float_as_uint(mx));
+    if (lane == 0) wmax[w] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = wmax[0];
+        for (int q = 1; q < 8; ++q) m = fmaxf(m, wmax[q]);
+        if (m > 0.f) atomicMax(absmax, __float_as_uint(m));
+    }
 }
-
 
 // The cost epilogue shared by all tensor-core paths (the unfused GEMM, the
 // fused forward and the fused backward recompute): accumulator acc of row i,
