@@ -1,0 +1,35 @@
+"""The reference's C++ API on the engine (include/softdtw_b200/dropin.hpp):
+tests/cpp/conformance.cpp compares softdtw::b200::{sdtw_with_gradients,
+barycenter_objective} (fp32, GPU) with the unmodified reference's functions
+(T = double, CPU) and checks the reference's exception types and ledger
+semantics survive the drop-in."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "_bin", "conformance")
+REF_INC = "/root/reference/proj/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not mounted (GPU box)")
+def test_dropin_builds_against_reference_headers():
+    from paper_2602_17206_b200.build import build
+    build()
+    r = subprocess.run(["make", "-C", os.path.join(HERE, "cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-4000:]
+    assert os.path.exists(BIN)
+    ldd = subprocess.run(["ldd", BIN], capture_output=True, text=True).stdout
+    assert "libsdtw_b200.so" in ldd and "not found" not in ldd
+
+
+@pytest.mark.gpu
+def test_dropin_conformance_on_gpu():
+    if not os.path.exists(BIN):
+        pytest.fail("tests/cpp/_bin/conformance missing: build it where the reference is mounted "
+                    "(make -C tests/cpp or __graft_entry__.build())")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASS" in r.stdout
