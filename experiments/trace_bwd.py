@@ -9,7 +9,7 @@ S = (L + 31) // 32
 eng = Engine(0)
 g = torch.Generator(device="cuda").manual_seed(42)
 x = torch.randn((B, L, D), device="cuda", generator=g); y = torch.randn((B, L, D), device="cuda", generator=g)
-tr = torch.zeros(13 * B * S, dtype=torch.int64, device="cuda")
+tr = torch.zeros(40 * B * S, dtype=torch.int64, device="cuda")
 eng.lib.sdtw_debug_set_trace(eng.ctx, tr.data_ptr())
 for _ in range(2):
     tr.zero_()
@@ -24,7 +24,7 @@ print("pair0 strip start (bottom first):", np.round(st[0, ::-1][:8], 1))
 print("pair0 strip end (bottom first):", np.round(en[0, ::-1][:8], 1), "...", np.round(en[0, ::-1][-4:], 1))
 print("live tiles per strip (pair 0, bottom first):", nt[0, ::-1][:16].astype(int))
 print("mean live tiles per strip", nt.mean())
-evs = t[5 * B * S:].reshape(B, S, 8)
+evs = t[5 * B * S:13 * B * S].reshape(B, S, 8)
 def rel(e):
     v = evs[:, :, e]
     return np.where(v > 0, (v - bw[:, :, 0]) / 1e3, np.nan)

@@ -1,0 +1,33 @@
+# Backward event log (trace mode): per strip (time, chunk, kind) records.
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from bench import CONFIGS
+from paper_2602_17206_b200 import Engine
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+fused = len(sys.argv) > 2 and sys.argv[2] == "fused"
+B, L, D = cfg["B"], cfg["L"], cfg["D"]
+S = (L + 31) // 32
+eng = Engine(0)
+torch.manual_seed(0)
+x = torch.randn((B, L, D), device="cuda"); y = torch.randn((B, L, D), device="cuda")
+tr = torch.zeros(140 * B * S, dtype=torch.int64, device="cuda")
+for it in range(2):
+    eng.lib.sdtw_debug_set_trace(eng.ctx, tr.data_ptr() if it == 1 else None)
+    tr.zero_()
+    eng.sdtw_with_gradients(x, y, cfg["gamma"], fused=fused)
+    torch.cuda.synchronize()
+eng.lib.sdtw_debug_set_trace(eng.ctx, None)
+t = tr.cpu().numpy()
+evs = t[40 * B * S:88 * B * S].reshape(B, S, 16, 3)
+t0 = evs[..., 0][evs[..., 0] > 0].min()
+names = {1: "R+", 2: "R-", 3: "E+", 4: "E-"}
+b = 0
+for s in range(S - 1, max(-1, S - 9), -1):
+    line = []
+    for k in range(16):
+        tm, ch, kd = evs[b, s, k]
+        if tm == 0:
+            break
+        line.append(f"{names[int(kd)]}{int(ch)}@{(tm - t0) / 1e3:.1f}")
+    print(f"strip {s:3d}: " + " ".join(line))

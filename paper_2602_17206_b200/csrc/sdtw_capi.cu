@@ -622,16 +622,16 @@ struct Pipeline {
                 // every CTA holds 128 TMEM columns for its lifetime: at most
                 // 4 may be resident on an SM (the shared memory guarantees it)
                 static_assert(sdtw::Bwd4Smem<float, false, true>::kPerWarp * 4 > 233472 / 5,
-                              "fused backward CTA must not fit 5 per SM");
-                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat, ftc());
+                              "fused backward CTA must not fit 5 per SM");  // (per CTA: 2 warps)
+                LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, ftc());
             } else if (fused) {
                 auto kern = sdtw::sdtw_backward4_kernel<T, true>;
                 const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat, sdtw::FusedTcArgs{});
+                LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, sdtw::FusedTcArgs{});
             } else {
                 auto kern = sdtw::sdtw_backward4_kernel<T, false>;
                 const size_t smem = sdtw::Bwd4Smem<T, false>::kPerWarp * sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, 32, smem, B * S), 32, smem, A, stat, sdtw::FusedTcArgs{});
+                LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, sdtw::FusedTcArgs{});
             }
         }
         if (gx || gy) {

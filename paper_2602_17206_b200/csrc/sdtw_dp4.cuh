@@ -43,12 +43,13 @@ struct Bwd4Smem {
     // the M = 128 MMA read (harmlessly) into the probability slots after it
     static constexpr int kX = kTc ? kFtcMaxD * 32 * 4 / (int)sizeof(T) : 0;
     static constexpr int kSlot = 3 * 33 * 32;            // pd, pu, pl [jj][t], row 32 = dummy
-    static constexpr int kP = 3 * kSlot;                 // three probability tiles
+    static constexpr int kP = 6 * kSlot;                 // two groups of three probability tiles
     static constexpr int kE = 32 * 34;                   // E tile [t][jj] (even stride: conflict-free), column 32 = dummy
     static constexpr int kRing = (kFused && !kTc) ? 0 : 4 * 1024;  // skewed cost row groups (slot g & 3)
     static constexpr int kHalo = 6 * 32;                 // 3 top halos (h), S in, S out (+dummy)
     static constexpr int kBar = kTc ? 16 / (int)sizeof(T) + 2 : 0;  // 2 mbarriers + TMEM base (kTc)
-    static constexpr int kPerWarp = kX + kP + kE + kRing + kHalo + kBar;
+    static constexpr int kCtl = 64 / (int)sizeof(T);                 // 16 ints: warp hand-off block
+    static constexpr int kPerWarp = kX + kP + kE + kRing + kHalo + kBar + kCtl;  // per CTA (2 warps)
 };
 
 // Status words: (epoch << 32) | status.
@@ -98,7 +99,7 @@ __device__ __forceinline__ T bwd_cost(const DpArgs<T> &a, const T *ring, int b, 
 // is warp 0 of its CTA, so it owns TMEM lanes 0..31: its strip's 32 rows are
 // rows 0..31 of an M = 128 MMA whose other rows are don't-care.
 template <class T, bool kFused, bool kTc = false>
-__global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, unsigned long long *stat,
+__global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, unsigned long long *stat,
                                                             FusedTcArgs F)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
     using SM = Bwd4Smem<T, kFused, kTc>;
     using TG = Tagged<T>;
     const int t = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;  // 0: recompute helper (owns TMEM lanes 0..31), 1: E sweep
     uint8_t *xs = smem_raw;  // kTc: packed x rows of the strip
     T *base = reinterpret_cast<T *>(smem_raw) + SM::kX;
     // kTc: [0] MMA done, [1] operand copies landed; then the TMEM base
@@ -114,15 +116,19 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
     uint32_t tc_ph[2] = {0u, 0u};
     uint32_t tmem = 0;
     float tc_m2 = 0.f;
+    // warp hand-off block: [0] ticket, [1] requested window, [2] request
+    // sequence, [3] strip done, [4] E position, [5..6] window start of slot
+    // group g, [7..8] group state (0 empty, 1 computing, 2 ready)
+    volatile int *ctl = reinterpret_cast<volatile int *>(base + SM::kP + SM::kE + SM::kRing + SM::kHalo + SM::kBar);
     if constexpr (kTc) {
-        if (t == 0) {
+        if (threadIdx.x == 0) {
             tc::mbar_init(&tc_bar[0], 1);
             tc::mbar_init(&tc_bar[1], 1);
             tc::fence_barrier_init();
         }
-        tc::tmem_alloc<128>(&tc_tmem);
+        if (warp == 0) tc::tmem_alloc<128>(&tc_tmem);
         tc::tc_fence_before();
-        __syncwarp();
+        __syncthreads();
         tc::tc_fence_after();
         tmem = tc_tmem;
         tc_m2 = -2.0f * split_scale(A.absmax).inv;
@@ -139,7 +145,21 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
     const int ngroups_row = a.KK / 32;
     const FxScales fx = fx_scales(A.absmax, a.N, a.M);
     for (;;) {
-        const unsigned tk = warp_ticket(&a.tickets[1]);
+        if (warp == 1) {
+            const unsigned tk1 = warp_ticket(&a.tickets[1]);
+            if (t == 0) {
+                ctl[0] = (int)tk1;
+                ctl[1] = -1;
+                ctl[2] = 0;
+                ctl[3] = 0;
+                ctl[4] = a.C;
+                ctl[5] = ctl[6] = -1000;
+                ctl[7] = ctl[8] = 0;
+            }
+        }
+        __syncthreads();
+        const unsigned tk = (unsigned)ctl[0];
+        __syncthreads();
         if ((int)tk >= total) break;
         const int s = a.S - 1 - (int)tk / a.B, b = (int)tk % a.B;
         const int i = 32 * s + t + 1;
@@ -152,7 +172,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
         const unsigned long long *stat_below = stat + ((size_t)b * a.S + s + 1) * a.C;
         typename TG::Ent *sb_me = A.sbt + ((size_t)b * a.S + s) * a.M;
         const typename TG::Ent *sb_below = A.sbt + ((size_t)b * a.S + s + 1) * a.M;
-        if (A.trace && t == 0) A.trace[2 * ((size_t)a.B * a.S + (size_t)b * a.S + s)] = global_ns();
+        if (A.trace && t == 0 && warp == 1) A.trace[2 * ((size_t)a.B * a.S + (size_t)b * a.S + s)] = global_ns();
         int ntiles = 0;
         int nstored = 0;  // tiles of this strip in the store
         // cycle accounting (trace mode): [32 B S + 8 (b S + s) + e]: e = 0
@@ -166,14 +186,31 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                 c_mark = now;
             }
         };
-        auto ev = [&](int e) {
-            if (A.trace && t == 0 && e < 8)
-                A.trace[5 * (size_t)a.B * a.S + 8 * ((size_t)b * a.S + s) + e] = global_ns();
+        // event log (trace mode): up to 16 (time, chunk, kind) records per
+        // strip at [40 B S + 48 (b S + s) + 3 k]; kinds 1/2 recompute
+        // start/end, 3/4 E phase start/end
+        int nev = 0;
+        auto ev = [&](int kind, int chunk) {
+            if (A.trace && t == 0 && nev < 16) {
+                // E warp: [40 B S ..), helper: [88 B S ..)
+                unsigned long long *r = A.trace + (warp == 1 ? 40 : 88) * (size_t)a.B * a.S +
+                                        48 * ((size_t)b * a.S + s) + 3 * nev;
+                r[0] = global_ns();
+                r[1] = (unsigned long long)chunk;
+                r[2] = (unsigned long long)kind;
+                ++nev;
+            }
         };
         T e_right = T(0), pl_right = T(0), pd_right = T(0);
-        // P-tile cache: slot k holds chunk slot_c[k] (-1: none)
-        int slot_c0 = -1, slot_c1 = -1, slot_c2 = -1;
-        auto find_slot = [&](int cf) { return slot_c0 == cf ? 0 : slot_c1 == cf ? 1 : slot_c2 == cf ? 2 : -1; };
+        int grp = 0;  // slot group the helper is filling
+        // which group holds tile cf (state >= 1), -1 if none
+        auto group_of = [&](int cf) {
+            for (int g = 0; g < 2; ++g) {
+                const int w0 = ctl[5 + g];
+                if (ctl[7 + g] != 0 && cf <= w0 && cf > w0 - 3 && cf >= 0) return g;
+            }
+            return -1;
+        };
         // kTc: cost blocks of chunks cr, cr-1, .. (nt of them) -> skewed ring.
         // Operands: the strip's x rows (loaded once per strip) and the y
         // chunks, staged K-half by K-half in the probability slots (free
@@ -181,7 +218,8 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
         auto tc_costs = [&](int cr, int nt, bool &xl, int b_, int s_, int i_, bool rok, float xi) {
             if constexpr (kTc) {
                 const int dpad = F.dpad;
-                uint8_t *stage = reinterpret_cast<uint8_t *>(base);
+                // operand staging inside the target group's own slots (free)
+                uint8_t *stage = reinterpret_cast<uint8_t *>(base + kSlot * 3 * grp);
                 const uint32_t idesc = tc::idesc_f16_f32(128, 32);
                 const SplitScale sc = split_scale(A.absmax);
                 // raw fp32 staging after the three fp16 operand tiles (the
@@ -195,7 +233,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                     const int jz = 32 * (cr - z) + t;
                     yv3[z] = (z < nt && jz < a.M) ? (float)a.yn[(size_t)b_ * a.M + jz] : 0.f;
                 }
-                float *raw = reinterpret_cast<float *>(stage + 3 * 8192);
+                float *raw = reinterpret_cast<float *>(stage + 2 * 8192);  // <= 34 KB of the 38 KB group
                 const bool async_ok = (a.D & 3) == 0;
                 const float *xg = reinterpret_cast<const float *>(a.x) + (size_t)b_ * a.N * a.D;
                 const float *yg = reinterpret_cast<const float *>(a.y) + (size_t)b_ * a.M * a.D;
@@ -293,8 +331,10 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             }
         };
         // recompute tile cr and, speculatively, cr-1 and cr-2 (independent
-        // tiles in one skewed loop: ILP 3); tile cr - z lands in slot z
+        // tiles in one skewed loop: ILP 3); tile cr - z lands in slot z of
+        // group grp (helper warp only)
         auto recompute = [&](int cr) {
+            ev(1, cr);
             lap(5);
             const int wr = min(32, a.M - 32 * cr);
             const int nt = min(3, cr + 1);
@@ -360,7 +400,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                                 prob_cell<T>(d, u[z], lc[z], a.k, a.gln2, v, h, pd, pu, pl);
                             }
                             // inactive lanes write the dummy row: no divergent branch
-                            T *Pz = base + kSlot * z + (act ? jj : 32) * 32 + t;
+                            T *Pz = base + kSlot * (3 * grp + z) + (act ? jj : 32) * 32 + t;
                             Pz[0] = pd;
                             Pz[1056] = pu;
                             Pz[2112] = pl;
@@ -374,9 +414,94 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             }
             __syncwarp();
             lap(0);
-            slot_c0 = cr;
-            slot_c1 = nt > 1 ? cr - 1 : -1;
-            slot_c2 = nt > 2 ? cr - 2 : -1;
+            ev(2, cr);
+        };
+        // ---- helper side: serve a window request / extend the cache leftwards
+        auto pick_group = [&]() {
+            const int e_pos = ctl[4];
+            for (int g = 0; g < 2; ++g)
+                if (ctl[7 + g] == 0 || ctl[5 + g] - 2 > e_pos) return g;  // empty or passed by E
+            return ctl[5] < ctl[6] ? 0 : 1;                                 // else the leftmost (speculative)
+        };
+        auto serve = [&](int cr) {
+            int g = -1;
+            if (t == 0) g = group_of(cr) >= 0 ? -1 : pick_group();
+            g = __shfl_sync(kFull, g, 0);
+            if (g < 0) return false;
+            if (t == 0) {
+                ctl[7 + g] = 0;
+                __threadfence_block();
+                ctl[5 + g] = cr;
+                __threadfence_block();
+                ctl[7 + g] = 1;
+            }
+            __syncwarp();
+            grp = g;
+            recompute(cr);
+            __threadfence_block();
+            __syncwarp();
+            if (t == 0) ctl[7 + g] = 2;
+            return true;
+        };
+        auto speculate = [&]() {
+            int cn = -1;
+            if (t == 0) {
+                int w = 1 << 30;
+                for (int g = 0; g < 2; ++g)
+                    if (ctl[7 + g] != 0) w = min(w, ctl[5 + g]);
+                const int e_pos = ctl[4];
+                if (w != (1 << 30) && w - 3 >= 0 && w - 3 <= e_pos) {
+                    // only into a group E no longer needs
+                    bool free_g = false;
+                    for (int g = 0; g < 2; ++g)
+                        free_g |= ctl[7 + g] == 0 || ctl[5 + g] - 2 > e_pos;
+                    if (free_g) cn = w - 3;
+                }
+            }
+            cn = __shfl_sync(kFull, cn, 0);
+            return cn >= 0 && serve(cn);
+        };
+        // ---- E side: ask for a window / wait for a tile's probabilities
+        auto request = [&](int cr) {
+            int have = 0;
+            if (t == 0) have = group_of(cr) >= 0;
+            if (__shfl_sync(kFull, have, 0)) return;
+            if (t == 0) {
+                ctl[1] = cr;
+                __threadfence_block();
+                ctl[2] = ctl[2] + 1;
+            }
+            __syncwarp();
+        };
+        auto tile_P = [&](int cf) -> T * {
+            bool requested = false;
+            unsigned polls = 0;
+            for (;;) {
+                int g = -1, st = 0, w0 = 0;
+                if (t == 0) {
+                    g = group_of(cf);
+                    if (g >= 0) {
+                        st = ctl[7 + g];
+                        w0 = ctl[5 + g];
+                    }
+                }
+                g = __shfl_sync(kFull, g, 0);
+                st = __shfl_sync(kFull, st, 0);
+                w0 = __shfl_sync(kFull, w0, 0);
+                if (g >= 0 && st == 2) {
+                    __threadfence_block();
+                    return base + kSlot * (3 * g + (w0 - cf));
+                }
+                if (g < 0 && !requested) {
+                    request(cf);
+                    requested = true;
+                }
+                __nanosleep(20);
+                if (++polls > (1u << 26)) {
+                    if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
+                    return base;
+                }
+            }
         };
         auto advance = [&](int) {};
         auto dead_chunk = [&](int cd) {
@@ -384,8 +509,41 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             if (t < w) TG::store(sb_me + 32 * cd + t, T(0), epoch);
             if (t == 0) put_status(stat_me + cd, kTileDead, epoch);
         };
-        int c = a.C - 1;
+        if (warp == 0) {
+            // ---- recompute helper: serve requests, speculate one window ahead
+            int my_seq = 0;
+            unsigned idle = 0;
+            for (;;) {
+                int seq = 0, done = 0, req = -1;
+                if (t == 0) {
+                    seq = ctl[2];
+                    done = ctl[3];
+                    req = ctl[1];
+                }
+                seq = __shfl_sync(kFull, seq, 0);
+                done = __shfl_sync(kFull, done, 0);
+                req = __shfl_sync(kFull, req, 0);
+                if (seq != my_seq) {
+                    my_seq = seq;
+                    serve(req);
+                    idle = 0;
+                    continue;
+                }
+                if (done) break;
+                if (speculate()) {
+                    idle = 0;
+                    continue;
+                }
+                __nanosleep(64);
+                if (++idle > (1u << 26)) {
+                    if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
+                    break;
+                }
+            }
+        }
+        int c = warp == 1 ? a.C - 1 : -1;
         while (c >= 0) {
+            if (t == 0) ctl[4] = c;
             const bool has_end = bottom && c == a.C - 1;
             const bool live_right = has_end || __any_sync(kFull, e_right != T(0));
             if (!live_right) {
@@ -426,7 +584,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                 if (st0 >= kTileCommit) {
                     // the strip below has no evidence yet: recompute early (and
                     // say so one level up), then wait for its verdict
-                    if (find_slot(c) < 0) recompute(c);
+                    request(c);
                     if (st0 + 1 < kTileCommit + kSpecDepth && t == 0) put_status(stat_me + c, st0 + 1, epoch);
                     polls = 0;
                     lap(5);
@@ -457,10 +615,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             if (t == 0) put_status(stat_me + c, hinted ? kTileHint : kTileCommit, epoch);
             const int j0 = 32 * c + 1;
             const int width = min(32, a.M - 32 * c);
-            ev(3 + 2 * min(ntiles, 1));
-            if (find_slot(c) < 0) recompute(c);
-            ev(4 + 2 * min(ntiles, 1));
-            T *Pc = base + kSlot * find_slot(c);
+            T *Pc = tile_P(c);
             // ---- phase E with 8-column hand-offs --------------------------
             const bool has_end_tile = bottom && c == a.C - 1;
             T s_prev = T(0);
@@ -471,6 +626,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             // sub-group's probabilities loaded up front (no shared load on the
             // step chain), branch-free steps; S published as soon as lane 0
             // completes a group of 8 columns (after step 6 of a sub-group).
+            ev(3, c);
             int pub_next = 0;  // next 8-column group (from the right) to publish
             auto publish = [&](int done) {
                 // groups k with all columns done (or the tile's last partial group)
@@ -568,6 +724,7 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             }
             __syncwarp();
             lap(2);
+            ev(4, c);
             // final status: does any S go up?  (stops the spread of hints over
             // tiles whose inputs turned out to be exactly zero)
             const bool s_nz = __any_sync(kFull, t < width && sout_s[t] != T(0));
@@ -609,6 +766,9 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
             --c;
         }
         lap(5);
+        if (warp == 1 && t == 0) ctl[3] = 1;  // strip done: release the helper
+        __syncthreads();
+        if (warp == 0) continue;
         if (t == 0) A.strip_tiles[(size_t)b * a.S + s] = nstored;
         if (A.trace && t == 0)
             for (int e = 0; e < 8; ++e)
@@ -620,8 +780,8 @@ __global__ void __launch_bounds__(32, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
     }
     if constexpr (kTc) {
         tc::tc_fence_before();
-        __syncwarp();
-        tc::tmem_dealloc<128>(tmem);
+        __syncthreads();
+        if (warp == 0) tc::tmem_dealloc<128>(tmem);
     }
 }
 
