@@ -236,6 +236,201 @@ __device__ __forceinline__ void half_chunk_store(const HalfChunk &h, float sc, u
 }
 
 // ---------------------------------------------------------------------------
+// One strip of a slot (super-strip of 4 strips, warp w = strip w): the v3
+// forward step body with the slot's shared-memory hand-off between its strips
+// and the tagged L2 halo for strip 0.  `fill(G, lap)` makes the costs of
+// skewed group G available in `ring` (two 1024-float groups, slot G & 1):
+// the fused kernel's TMEM epilogue or the unfused kernel's cp.async of the
+// cost tensor.
+// ---------------------------------------------------------------------------
+template <class Fill>
+__device__ __forceinline__ void slot_strip_forward(const Dp3Args<float> &A, int b, int s, int w, unsigned base,
+                                                   float *ring, float *halo_s, unsigned *rd,
+                                                   unsigned long long (*hx)[kFtcHx], Fill &&fill)
+{
+    using TG = Tagged<float>;
+    const DpArgs<float> &a = A.a;
+    const int t = threadIdx.x & 31;
+    const unsigned epoch = A.epoch;
+    const unsigned Mu = (unsigned)a.M;
+    const float inf = Num<float>::inf();
+            const int row = 32 * s + t + 1;
+    const bool row_ok = row <= a.N;
+    // trace: [16 B S + 4 (b S + s) + e]: e = 0 ticket, 1 first 32 columns
+    // done, 2 half the columns done, 3 end
+    unsigned long long *trc = A.trace ? A.trace + 16 * (size_t)a.B * a.S + 4 * ((size_t)b * a.S + s) : nullptr;
+    if (trc && t == 0) trc[0] = global_ns();
+    // cycle accounting (trace mode): [24 B S + 8 (b S + s) + e]:
+    // e = 0 cost-tile wait, 1 epilogue, 2 halo wait, 3 back-pressure, 4 steps
+    long long cyc[5] = {0, 0, 0, 0, 0};
+    long long c_mark = trc ? clock64() : 0;
+    auto lap = [&](int e) {
+if (trc) {
+    const long long now = clock64();
+    cyc[e] += now - c_mark;
+    c_mark = now;
+}
+    };
+    const bool top_global = w == 0;             // halo from the previous super-strip (L2)
+    const bool pub_local = w < 3 && s + 1 < a.S;  // hand h to the strip below in smem
+    float h_prev = 0.f, l_carry = 0.f;
+    double lacc = 0.0;
+    float gdiag = 0.f;
+    const int kdiag = 32 * s + 2 * t;
+    const typename TG::Ent *hb_top = A.hbt + ((size_t)b * a.S + (s - 1)) * a.M;
+    typename TG::Ent *hb_me = A.hbt + ((size_t)b * a.S + s) * a.M;
+    const unsigned long long *hx_up = w > 0 ? hx[w - 1] : nullptr;
+    unsigned long long *hx_me = w < 3 ? hx[w] : hx[0];
+    const int steps = a.M + 31;
+    const bool r1 = row == 1;  // lane 0 of a pair's first strip: R(0, j) = inf
+    const bool has_rowN = 32 * (s + 1) >= a.N;
+    unsigned long long pf_w = 0;
+    int pf_kb = -1;
+    for (int k0 = 0; k0 < steps; k0 += 32) {
+const int G = k0 >> 5;
+__syncwarp();
+if (trc && t == 0 && (G == 1 || G == a.C / 2)) trc[G == 1 ? 1 : 2] = global_ns();
+fill(G, lap);
+const int cmin = k0 - 31, cmax = k0 + 31;
+const bool fixup = cmin <= 0 ||
+                   (a.bw != 0 && (32 * s - k0 - 31 < -a.bw || 32 * s + 62 - k0 > a.bw));
+const bool tail = (has_rowN && a.M > a.N && cmax >= a.N) || (a.N > a.M && cmax >= a.M - 1);
+float vck = 0.f;
+const float *rg = ring + (G & 1) * 1024;
+#pragma unroll 1
+for (int k8 = 0; k8 < 32; k8 += 8) {
+    const int kb = k0 + k8;
+    // ---- top halo for columns [kb, kb + 8): tagged entries,
+    // from L2 (strip 0 of the slot) or from the slot's ring
+    lap(4);
+    if (s > 0 && kb < a.M) {
+        const int nn = min(8, a.M - kb);
+        float hv = 0.f;
+        if (top_global) {
+            bool ok = t >= nn;
+            if (!ok) {
+                const unsigned long long w8 = (pf_kb == kb) ? pf_w : TG::load_raw(hb_top + kb + t);
+                ok = (unsigned)(w8 >> 32) == epoch;
+                hv = __uint_as_float((unsigned)(w8 & 0xffffffffull));
+            }
+            if (!__all_sync(kFull, ok)) hv = poll_entries<float>(hb_top + kb, nn, epoch, t);
+            const int kb2 = kb + 8;
+            if (kb2 < a.M && t < min(8, a.M - kb2)) {
+                pf_w = TG::load_raw(hb_top + kb2 + t);
+                pf_kb = kb2;
+            }
+        } else {
+            const unsigned pos = base + (unsigned)(kb + t);
+            bool ok = t >= nn;
+            unsigned polls = 0;
+            for (;;) {
+                if (!ok) {
+                    const unsigned long long e8 = ld_volatile_u64(hx_up + (pos & (kFtcHx - 1)));
+                    ok = (unsigned)(e8 >> 32) == pos;
+                    hv = __uint_as_float((unsigned)(e8 & 0xffffffffull));
+                }
+                if (__all_sync(kFull, ok)) break;
+                if (++polls > (1u << 28)) {
+                    if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
+                    break;
+                }
+            }
+        }
+        if (t < nn) halo_s[(kb + t) & 31] = hv;
+        __syncwarp();
+        if (!top_global && t == 0) st_volatile_u32(&rd[w], base + (unsigned)(kb + nn));
+    }
+    lap(2);
+    // ---- back-pressure: the strip below must have consumed the
+    // hand-off entries these 8 steps overwrite
+    if (pub_local) {
+        const int cw = kb + 8 - 31;  // columns [.., cw) final after this sub-group
+        if (cw > 0) {
+            const unsigned need = base + (unsigned)cw - (unsigned)kFtcHx;
+            unsigned polls = 0;
+            while ((int)(ld_volatile_u32(&rd[w + 1]) - need) < 0) {
+                if (++polls > (1u << 28)) {
+                    if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
+                    break;
+                }
+            }
+        }
+    }
+    lap(3);
+    // two copies of the 8 steps: with the boundary / band / tail
+    // fix-ups, and the plain branch-free one (warp-uniform choice)
+    auto steps8 = [&](auto fix_tag) {
+        constexpr bool kFix = decltype(fix_tag)::value;
+        // the 8 halo values and costs up front: no shared load
+        // on the step's dependency chain
+        float hsv[8], dvv[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            hsv[kk] = halo_s[k8 + kk];
+            dvv[kk] = rg[(k8 + kk) * 32 + t];
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int k = kb + kk;
+            const int kl = k8 + kk;
+            const float src = (t == 31) ? hsv[kk] : h_prev;
+            const float uu = __shfl_sync(kFull, src, (t + 31) & 31);
+            const int col = k - t;
+            const bool active = row_ok && col >= 0 && col < a.M;
+            const float d = dvv[kk];
+            float g, v, h;
+            fwd_cell<float>(d, uu, l_carry, a.k, a.gln2, g, v, h);
+            // row 1 in every group (three selects, no branch)
+            g = r1 ? d : g;
+            v = r1 ? -inf : v;
+            h = r1 ? d : h;
+            if constexpr (kFix) {
+                if (fixup) {
+                    const bool j1 = col == 0;
+                    g = j1 ? d : g;
+                    v = r1 ? -inf : (j1 ? d : v);
+                    h = j1 ? -inf : h;
+                    if (a.bw != 0 && !in_band(row, col + 1, a.bw)) {
+                        g = inf; v = inf; h = inf;
+                    }
+                }
+                if (tail && active) {
+                    const int i = row, j = col + 1;
+                    if (i == a.N && j > a.N) lacc += (double)h;
+                    if (j == a.M && i > a.M) lacc += (double)v;
+                }
+            }
+            gdiag = (active && k == kdiag) ? g : gdiag;
+            vck = (kl == ((t - 1) & 31)) ? v : vck;
+            l_carry = v;
+            h_prev = h;
+            if (!FTC_EXP_NO_STG) TG::store_if(hb_me + col, h, epoch, t == 31 && active);
+            const unsigned pos = base + (unsigned)col;
+            if (!FTC_EXP_NO_HX)
+                st_shared_u64_if(hx_me + (pos & (kFtcHx - 1)),
+                                 ((unsigned long long)pos << 32) | __float_as_uint(h),
+                                 pub_local && t == 31 && active);
+        }
+    };
+    if (fixup || tail) steps8(std::true_type{});
+    else steps8(std::false_type{});
+}
+const int bidx = (t == 0) ? G : (G - 1);
+const int jb = 32 * (bidx + 1);
+if (bidx >= 0 && jb < a.M && row_ok) a.vc[((size_t)b * a.C + bidx) * a.N + (row - 1)] = vck;
+    }
+    if (t == 0) st_volatile_u32(&rd[w], base + Mu);
+    if (trc && t == 0) trc[3] = global_ns();
+    lap(4);
+    if (trc && t == 0)
+for (int e = 0; e < 5; ++e)
+    A.trace[24 * (size_t)a.B * a.S + 8 * ((size_t)b * a.S + s) + e] = (unsigned long long)cyc[e];
+    lacc += (double)gdiag;
+    for (int off = 16; off > 0; off >>= 1) lacc += __shfl_xor_sync(kFull, lacc, off);
+    if (t == 0) a.lpart[(size_t)b * a.S + s] = lacc;
+}
+
+// ---------------------------------------------------------------------------
 // Fused forward (fp32).  384 threads: warps 0-3 slot 0 DP, 4-7 slot 1 DP,
 // 8-9 / 10-11 the producer pair of slot 0 / 1 (the first of a pair takes the
 // tickets and issues the MMAs).  Tickets over super-strips (strip-major,
@@ -371,44 +566,12 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
                 if (t == 0) st_volatile_u32(&sh.rd[p][w], base + Mu);
                 continue;
             }
-            const int row = 32 * s + t + 1;
-            const bool row_ok = row <= a.N;
-            // trace: [16 B S + 4 (b S + s) + e]: e = 0 ticket, 1 first 32 columns
-            // done, 2 half the columns done, 3 end
-            unsigned long long *trc = A.trace ? A.trace + 16 * (size_t)a.B * a.S + 4 * ((size_t)b * a.S + s) : nullptr;
-            if (trc && t == 0) trc[0] = global_ns();
-            // cycle accounting (trace mode): [24 B S + 8 (b S + s) + e]:
-            // e = 0 cost-tile wait, 1 epilogue, 2 halo wait, 3 back-pressure, 4 steps
-            long long cyc[5] = {0, 0, 0, 0, 0};
-            long long c_mark = trc ? clock64() : 0;
-            auto lap = [&](int e) {
-                if (trc) {
-                    const long long now = clock64();
-                    cyc[e] += now - c_mark;
-                    c_mark = now;
-                }
-            };
-            const float xi = row_ok ? a.xn[(size_t)b * a.N + row - 1] : 0.f;
-            const bool top_global = w == 0;             // halo from the previous super-strip (L2)
-            const bool pub_local = w < 3 && s + 1 < a.S;  // hand h to the strip below in smem
-            float h_prev = 0.f, l_carry = 0.f;
-            double lacc = 0.0;
-            float gdiag = 0.f;
-            const int kdiag = 32 * s + 2 * t;
-            const typename TG::Ent *hb_top = A.hbt + ((size_t)b * a.S + (s - 1)) * a.M;
-            typename TG::Ent *hb_me = A.hbt + ((size_t)b * a.S + s) * a.M;
-            const unsigned long long *hx_up = w > 0 ? sh.hx[p][w - 1] : nullptr;
-            unsigned long long *hx_me = w < 3 ? sh.hx[p][w] : sh.hx[p][0];
-            const int steps = a.M + 31;
-            const bool r1 = row == 1;  // lane 0 of a pair's first strip: R(0, j) = inf
-            const bool has_rowN = 32 * (s + 1) >= a.N;
-            unsigned long long pf_w = 0;
-            int pf_kb = -1;
+            const int row_f = 32 * s + t + 1;
+            const float xi = row_f <= a.N ? a.xn[(size_t)b * a.N + row_f - 1] : 0.f;
             float yn_next = t < a.M ? a.yn[(size_t)b * a.M + t] : 0.f;
-            for (int k0 = 0; k0 < steps; k0 += 32) {
-                const int G = k0 >> 5;
-                __syncwarp();
-                if (trc && t == 0 && (G == 1 || G == a.C / 2)) trc[G == 1 ? 1 : 2] = global_ns();
+            const bool row_ok = row_f <= a.N;
+            const int row = row_f;
+            auto fill = [&](int G, auto &lap) {
                 if (G < a.C) {
                     // cost chunk G: TMEM quarter -> epilogue -> skewed ring
                     const unsigned uu = u + G;
@@ -446,143 +609,8 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
                     __syncwarp();
                     lap(1);
                 }
-                const int cmin = k0 - 31, cmax = k0 + 31;
-                const bool fixup = cmin <= 0 ||
-                                   (a.bw != 0 && (32 * s - k0 - 31 < -a.bw || 32 * s + 62 - k0 > a.bw));
-                const bool tail = (has_rowN && a.M > a.N && cmax >= a.N) || (a.N > a.M && cmax >= a.M - 1);
-                float vck = 0.f;
-                const float *rg = ring + (G & 1) * 1024;
-#pragma unroll 1
-                for (int k8 = 0; k8 < 32; k8 += 8) {
-                    const int kb = k0 + k8;
-                    // ---- top halo for columns [kb, kb + 8): tagged entries,
-                    // from L2 (strip 0 of the slot) or from the slot's ring
-                    lap(4);
-                    if (s > 0 && kb < a.M) {
-                        const int nn = min(8, a.M - kb);
-                        float hv = 0.f;
-                        if (top_global) {
-                            bool ok = t >= nn;
-                            if (!ok) {
-                                const unsigned long long w8 = (pf_kb == kb) ? pf_w : TG::load_raw(hb_top + kb + t);
-                                ok = (unsigned)(w8 >> 32) == epoch;
-                                hv = __uint_as_float((unsigned)(w8 & 0xffffffffull));
-                            }
-                            if (!__all_sync(kFull, ok)) hv = poll_entries<float>(hb_top + kb, nn, epoch, t);
-                            const int kb2 = kb + 8;
-                            if (kb2 < a.M && t < min(8, a.M - kb2)) {
-                                pf_w = TG::load_raw(hb_top + kb2 + t);
-                                pf_kb = kb2;
-                            }
-                        } else {
-                            const unsigned pos = base + (unsigned)(kb + t);
-                            bool ok = t >= nn;
-                            unsigned polls = 0;
-                            for (;;) {
-                                if (!ok) {
-                                    const unsigned long long e8 = ld_volatile_u64(hx_up + (pos & (kFtcHx - 1)));
-                                    ok = (unsigned)(e8 >> 32) == pos;
-                                    hv = __uint_as_float((unsigned)(e8 & 0xffffffffull));
-                                }
-                                if (__all_sync(kFull, ok)) break;
-                                if (++polls > (1u << 28)) {
-                                    if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
-                                    break;
-                                }
-                            }
-                        }
-                        if (t < nn) halo_s[(kb + t) & 31] = hv;
-                        __syncwarp();
-                        if (!top_global && t == 0) st_volatile_u32(&sh.rd[p][w], base + (unsigned)(kb + nn));
-                    }
-                    lap(2);
-                    // ---- back-pressure: the strip below must have consumed the
-                    // hand-off entries these 8 steps overwrite
-                    if (pub_local) {
-                        const int cw = kb + 8 - 31;  // columns [.., cw) final after this sub-group
-                        if (cw > 0) {
-                            const unsigned need = base + (unsigned)cw - (unsigned)kFtcHx;
-                            unsigned polls = 0;
-                            while ((int)(ld_volatile_u32(&sh.rd[p][w + 1]) - need) < 0) {
-                                if (++polls > (1u << 28)) {
-                                    if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
-                                    break;
-                                }
-                            }
-                        }
-                    }
-                    lap(3);
-                    // two copies of the 8 steps: with the boundary / band / tail
-                    // fix-ups, and the plain branch-free one (warp-uniform choice)
-                    auto steps8 = [&](auto fix_tag) {
-                        constexpr bool kFix = decltype(fix_tag)::value;
-                        // the 8 halo values and costs up front: no shared load
-                        // on the step's dependency chain
-                        float hsv[8], dvv[8];
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            hsv[kk] = halo_s[k8 + kk];
-                            dvv[kk] = rg[(k8 + kk) * 32 + t];
-                        }
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            const int k = kb + kk;
-                            const int kl = k8 + kk;
-                            const float src = (t == 31) ? hsv[kk] : h_prev;
-                            const float uu = __shfl_sync(kFull, src, (t + 31) & 31);
-                            const int col = k - t;
-                            const bool active = row_ok && col >= 0 && col < a.M;
-                            const float d = dvv[kk];
-                            float g, v, h;
-                            fwd_cell<float>(d, uu, l_carry, a.k, a.gln2, g, v, h);
-                            // row 1 in every group (three selects, no branch)
-                            g = r1 ? d : g;
-                            v = r1 ? -inf : v;
-                            h = r1 ? d : h;
-                            if constexpr (kFix) {
-                                if (fixup) {
-                                    const bool j1 = col == 0;
-                                    g = j1 ? d : g;
-                                    v = r1 ? -inf : (j1 ? d : v);
-                                    h = j1 ? -inf : h;
-                                    if (a.bw != 0 && !in_band(row, col + 1, a.bw)) {
-                                        g = inf; v = inf; h = inf;
-                                    }
-                                }
-                                if (tail && active) {
-                                    const int i = row, j = col + 1;
-                                    if (i == a.N && j > a.N) lacc += (double)h;
-                                    if (j == a.M && i > a.M) lacc += (double)v;
-                                }
-                            }
-                            gdiag = (active && k == kdiag) ? g : gdiag;
-                            vck = (kl == ((t - 1) & 31)) ? v : vck;
-                            l_carry = v;
-                            h_prev = h;
-                            if (!FTC_EXP_NO_STG) TG::store_if(hb_me + col, h, epoch, t == 31 && active);
-                            const unsigned pos = base + (unsigned)col;
-                            if (!FTC_EXP_NO_HX)
-                                st_shared_u64_if(hx_me + (pos & (kFtcHx - 1)),
-                                                 ((unsigned long long)pos << 32) | __float_as_uint(h),
-                                                 pub_local && t == 31 && active);
-                        }
-                    };
-                    if (fixup || tail) steps8(std::true_type{});
-                    else steps8(std::false_type{});
-                }
-                const int bidx = (t == 0) ? G : (G - 1);
-                const int jb = 32 * (bidx + 1);
-                if (bidx >= 0 && jb < a.M && row_ok) a.vc[((size_t)b * a.C + bidx) * a.N + (row - 1)] = vck;
-            }
-            if (t == 0) st_volatile_u32(&sh.rd[p][w], base + Mu);
-            if (trc && t == 0) trc[3] = global_ns();
-            lap(4);
-            if (trc && t == 0)
-                for (int e = 0; e < 5; ++e)
-                    A.trace[24 * (size_t)a.B * a.S + 8 * ((size_t)b * a.S + s) + e] = (unsigned long long)cyc[e];
-            lacc += (double)gdiag;
-            for (int off = 16; off > 0; off >>= 1) lacc += __shfl_xor_sync(kFull, lacc, off);
-            if (t == 0) a.lpart[(size_t)b * a.S + s] = lacc;
+            };
+            slot_strip_forward(A, b, s, w, base, ring, halo_s, sh.rd[p], sh.hx[p], fill);
             u += (unsigned)a.C;
         }
     }
