@@ -517,11 +517,16 @@ def run_engine_arm(args, cfg):
     if dom in ("forward", "backward"):
         mufu = MUFU_FWD if dom == "forward" else MUFU_BWD
         ach = mufu * cells_per_rank / (per_step[dom] / 1e3) / 1e9
-        roofline = {"bound": "sfu", "kernel": f"sdtw_{dom}_kernel", "achieved": ach,
+        kname = {"forward": "sdtw_forward_tc_kernel" if fused else "sdtw_forward3_kernel",
+                 "backward": "sdtw_backward4_kernel"}[dom]
+        roofline = {"bound": "sfu", "kernel": kname, "achieved": ach,
                     "peak": mufu_peak, "unit": "GMUFU-op/s", "frac": ach / mufu_peak,
                     "traffic": _traffic(args, dom),
                     "algorithmic": f"{mufu} MUFU/cell x {cells_per_rank} cells per launch "
-                                   "(SURVEY.md §8(d))",
+                                   "(SURVEY.md §8(d)); the backward computes only the tiles "
+                                   "whose E is not exactly zero, so its dense-equivalent rate "
+                                   "is reported" if dom == "backward" else
+                                   f"{mufu} MUFU/cell x {cells_per_rank} cells per launch (SURVEY.md §8(d))",
                     "peak_basis": f"{SM_COUNT} SM x {MUFU_PER_CLK_SM} MUFU/clk x {sm_mhz} MHz "
                                   f"(sm_max_mhz, {src})",
                     "share_of_step": per_step[dom] / (total_ms / args.steps)}
@@ -529,14 +534,14 @@ def run_engine_arm(args, cfg):
         flop = 2 * 2 * cells_per_rank * D
         ach = flop / (per_step[dom] / 1e3) / 1e12
         pk = float(peaks.get("bf16_tflops", 1590.0))
-        roofline = {"bound": "tensor", "kernel": "grad_contract_kernel", "achieved": ach,
+        roofline = {"bound": "tensor", "kernel": "contract_ordered_kernel", "achieved": ach,
                     "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
                     "share_of_step": per_step[dom] / (total_ms / args.steps)}
     elif dom == "costs":
         byt = 4 * cells_per_rank
         ach = byt / (per_step[dom] / 1e3) / 1e9
         pk = float(peaks.get("hbm_gbs", 6650.0))
-        roofline = {"bound": "hbm", "kernel": "cost_skewed_kernel", "achieved": ach, "peak": pk,
+        roofline = {"bound": "hbm", "kernel": "cost_gemm_tc_kernel", "achieved": ach, "peak": pk,
                     "unit": "GB/s", "frac": ach / pk, "traffic": None,
                     "share_of_step": per_step[dom] / (total_ms / args.steps)}
 
