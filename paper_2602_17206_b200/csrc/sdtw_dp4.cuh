@@ -34,6 +34,9 @@ namespace sdtw {
 // deep at most, so the recompute leaves the critical path without
 // cascading up whole columns.
 enum : unsigned { kTileDead = 1u, kTileHint = 2u, kTileLive = 3u, kTileCommit = 4u };
+#ifndef BWD_STATUS_SLEEP_NS
+#define BWD_STATUS_SLEEP_NS 32
+#endif
 constexpr unsigned kSpecDepth = 2;
 
 template <class T, bool kFused, bool kTc = false>
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                 unsigned polls = 0;
                 lap(5);
                 while (!__shfl_sync(kFull, st, 0)) {  // chunk c's status must be known
-                    __nanosleep(32);
+                    if (BWD_STATUS_SLEEP_NS > 0) __nanosleep(BWD_STATUS_SLEEP_NS);
                     if (cc >= 0 && st == 0) st = get_status(stat_below + cc, epoch);
                     if (++polls > (1u << 26)) {
                         if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
@@ -589,7 +592,7 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                     polls = 0;
                     lap(5);
                     while (st0 >= kTileCommit) {
-                        __nanosleep(64);
+                        if (BWD_STATUS_SLEEP_NS > 0) __nanosleep(2 * BWD_STATUS_SLEEP_NS);
                         st0 = __shfl_sync(kFull, get_status(stat_below + c, epoch), 0);
                         if (++polls > (1u << 26)) {
                             if (t == 0) atomicAdd(&g_sdtw_wait_timeouts, 1);
