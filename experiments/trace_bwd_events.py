@@ -21,7 +21,7 @@ eng.lib.sdtw_debug_set_trace(eng.ctx, None)
 t = tr.cpu().numpy()
 evs = t[40 * B * S:88 * B * S].reshape(B, S, 16, 3)
 t0 = evs[..., 0][evs[..., 0] > 0].min()
-names = {1: "R+", 2: "R-", 3: "E+", 4: "E-"}
+names = {1: "R+", 2: "R-", 3: "E+", 4: "E-", 5: "X"}
 b = 0
 for s in range(S - 1, max(-1, S - 9), -1):
     line = []
@@ -31,3 +31,11 @@ for s in range(S - 1, max(-1, S - 9), -1):
             break
         line.append(f"{names[int(kd)]}{int(ch)}@{(tm - t0) / 1e3:.1f}")
     print(f"strip {s:3d}: " + " ".join(line))
+    hl = []
+    hev = t[88 * B * S:136 * B * S].reshape(B, S, 16, 3)
+    for k in range(16):
+        tm, ch, kd = hev[b, s, k]
+        if tm == 0:
+            break
+        hl.append(f"{names[int(kd)]}{int(ch)}@{(tm - t0) / 1e3:.1f}")
+    print(f"   helper: " + " ".join(hl))

@@ -453,6 +453,18 @@ struct Pipeline {
         int occ = 0;
         CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+        if (std::getenv("SDTW_DEBUG_OCC")) {
+            std::fprintf(stderr, "[sdtw] occupancy %d blocks/SM (threads %d, smem %zu)\n", occ, threads, smem);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kern);
+            std::fprintf(stderr, "[sdtw]   regs %d static smem %zu local %zu maxthreads %d\n", fa.numRegs,
+                         fa.sharedSizeBytes, fa.localSizeBytes, fa.maxThreadsPerBlock);
+            for (size_t kb = 90; kb <= 114; kb += 4) {
+                int o = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, kb * 1024);
+                std::fprintf(stderr, "[sdtw]   %zu KB -> %d\n", kb, o);
+            }
+        }
         if (occ < 1) fail(SDTW_ECUDA, "DP kernel does not fit on an SM");
         const int wpc = threads / 32;
         const int need = (work_warps + wpc - 1) / wpc;
@@ -618,12 +630,13 @@ struct Pipeline {
             Phase ph(ctx, 3);
             if (tc_fused) {
                 auto kern = sdtw::sdtw_backward4_kernel<T, false, true>;
-                const size_t smem = sdtw::Bwd4Smem<T, false, true>::kPerWarp * sizeof(T);
-                // every CTA holds 128 TMEM columns for its lifetime: at most
-                // 4 may be resident on an SM (the shared memory guarantees it)
-                static_assert(sdtw::Bwd4Smem<float, false, true>::kPerWarp * 4 > 233472 / 5,
-                              "fused backward CTA must not fit 5 per SM");  // (per CTA: 2 warps)
-                LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, ftc());
+                constexpr int kW = sdtw::bwd_workers<true>();
+                const size_t smem = kW * sdtw::Bwd4Smem<T, false, true>::kWorkerBytes;
+                // TMEM-using kernels run one CTA per SM (measured with the
+                // occupancy API), so the CTA carries kW workers (2 x 128 columns)
+                static_assert(kW * sdtw::Bwd4Smem<float, false, true>::kWorkerBytes <= 232448,
+                              "fused backward workers must fit one CTA");
+                LAUNCH(ctx, kern, persistent_grid(kern, 64 * kW, smem, 2 * B * S), 64 * kW, smem, A, stat, ftc());
             } else if (fused) {
                 auto kern = sdtw::sdtw_backward4_kernel<T, true>;
                 const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);

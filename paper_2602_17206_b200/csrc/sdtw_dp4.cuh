@@ -52,7 +52,9 @@ struct Bwd4Smem {
     static constexpr int kHalo = 6 * 32;                 // 3 top halos (h), S in, S out (+dummy)
     static constexpr int kBar = kTc ? 16 / (int)sizeof(T) + 2 : 0;  // 2 mbarriers + TMEM base (kTc)
     static constexpr int kCtl = 64 / (int)sizeof(T);                 // 16 ints: warp hand-off block
-    static constexpr int kPerWarp = kX + kP + kE + kRing + kHalo + kBar + kCtl;  // per CTA (2 warps)
+    static constexpr int kPerWarp = kX + kP + kE + kRing + kHalo + kBar + kCtl;  // per worker (2 warps)
+    // per-worker stride in bytes (operand images need 16-byte alignment)
+    static constexpr size_t kWorkerBytes = ((size_t)kPerWarp * sizeof(T) + 1023) / 1024 * 1024;
 };
 
 // Status words: (epoch << 32) | status.
@@ -101,18 +103,30 @@ __device__ __forceinline__ T bwd_cost(const DpArgs<T> &a, const T *ring, int b, 
 // the same skewed ring the unfused path fills from the cost tensor.  The warp
 // is warp 0 of its CTA, so it owns TMEM lanes 0..31: its strip's 32 rows are
 // rows 0..31 of an M = 128 MMA whose other rows are don't-care.
+// Workers: a worker = (recompute helper warp, E warp) on one strip at a time.
+// kTc kernels hold TMEM, which limits them to one CTA per SM, so a kTc CTA
+// carries two independent workers (helper w owns TMEM lane quarter w and the
+// rows 32 w .. of its M = 128 MMAs); other variants run one worker per CTA.
+template <bool kTc>
+constexpr int bwd_workers() { return kTc ? 2 : 1; }
+
 template <class T, bool kFused, bool kTc = false>
-__global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, unsigned long long *stat,
-                                                            FusedTcArgs F)
+__global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_kernel(Dp3Args<T> A,
+                                                                                   unsigned long long *stat,
+                                                                                   FusedTcArgs F)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
+    __shared__ uint32_t tmem_slot;
+    constexpr int kW = bwd_workers<kTc>();
     const DpArgs<T> &a = A.a;
     using SM = Bwd4Smem<T, kFused, kTc>;
     using TG = Tagged<T>;
     const int t = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;  // 0: recompute helper (owns TMEM lanes 0..31), 1: E sweep
-    uint8_t *xs = smem_raw;  // kTc: packed x rows of the strip
-    T *base = reinterpret_cast<T *>(smem_raw) + SM::kX;
+    const int wk = (threadIdx.x >> 5) % kW;    // worker
+    const int warp = (threadIdx.x >> 5) / kW;  // role: 0 recompute helper, 1 E sweep
+    uint8_t *wsm = smem_raw + (size_t)wk * SM::kWorkerBytes;
+    uint8_t *xs = wsm;  // kTc: packed x rows of the strip
+    T *base = reinterpret_cast<T *>(wsm) + SM::kX;
     // kTc: [0] MMA done, [1] operand copies landed; then the TMEM base
     uint64_t *tc_bar = reinterpret_cast<uint64_t *>(base + SM::kP + SM::kE + SM::kRing + SM::kHalo);
     uint32_t &tc_tmem = *reinterpret_cast<uint32_t *>(tc_bar + 2);
@@ -123,19 +137,21 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
     // sequence, [3] strip done, [4] E position, [5..6] window start of slot
     // group g, [7..8] group state (0 empty, 1 computing, 2 ready)
     volatile int *ctl = reinterpret_cast<volatile int *>(base + SM::kP + SM::kE + SM::kRing + SM::kHalo + SM::kBar);
+    (void)tc_tmem;
     if constexpr (kTc) {
-        if (threadIdx.x == 0) {
+        if (warp == 0 && t == 0) {
             tc::mbar_init(&tc_bar[0], 1);
             tc::mbar_init(&tc_bar[1], 1);
             tc::fence_barrier_init();
         }
-        if (warp == 0) tc::tmem_alloc<128>(&tc_tmem);
+        if (threadIdx.x < 32) tc::tmem_alloc<128 * kW>(&tmem_slot);
         tc::tc_fence_before();
         __syncthreads();
         tc::tc_fence_after();
-        tmem = tc_tmem;
+        tmem = tmem_slot + 128u * wk;  // this worker's 128 columns
         tc_m2 = -2.0f * split_scale(A.absmax).inv;
     }
+    const uint32_t tmem_lanes = (uint32_t)(32 * wk) << 16;  // lane quarter of the helper
     // probability tile slots k = 0..2 at base + kSlot k: pd, pu, pl [jj][t]
     constexpr int kSlot = SM::kSlot;
     T *et_s = base + SM::kP;
@@ -160,9 +176,9 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                 ctl[7] = ctl[8] = 0;
             }
         }
-        __syncthreads();
+        named_bar(1 + wk, 64);
         const unsigned tk = (unsigned)ctl[0];
-        __syncthreads();
+        named_bar(1 + wk, 64);
         if ((int)tk >= total) break;
         const int s = a.S - 1 - (int)tk / a.B, b = (int)tk % a.B;
         const int i = 32 * s + t + 1;
@@ -259,7 +275,10 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                 // chunk the K halves in order, 4 K steps of hi.hi, hi.lo,
                 // lo.hi each)
                 const int KH = dpad / 64, U = nt * KH;
-                const uint32_t xh = tc::smem_u32(xs), xlo = xh + 32u * dpad * 2;
+                // A = rows 32 wk .. 32 wk + 31 of an M = 128 operand: the
+                // descriptor starts 4 wk 8-row groups (SBO = 128 B) before the
+                // strip's rows; the other rows read neighbouring shared memory
+                const uint32_t xh = tc::smem_u32(xs) - 512u * wk, xlo = xh + 32u * dpad * 2;
                 auto unit_raw = [&](int u) {
                     const int z = u / KH, kh = u % KH;
                     raw_rows_async(raw + (u & 1) * 32 * 68, yg, a.D, 32 * (cr - z), 32, a.M, 64 * kh, 64, a.D, t);
@@ -317,7 +336,7 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
                 lap(7);
                 for (int z = 0; z < nt; ++z) {
                     float acc[32];
-                    tc::tmem_ld32(tmem + 32u * z, acc);
+                    tc::tmem_ld32(tmem + tmem_lanes + 32u * z, acc);
                     const int j0 = 32 * (cr - z);
                     const float yv = z == 0 ? yv3[0] : (z == 1 ? yv3[1] : yv3[2]);
 #pragma unroll
@@ -770,7 +789,7 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
         }
         lap(5);
         if (warp == 1 && t == 0) ctl[3] = 1;  // strip done: release the helper
-        __syncthreads();
+        named_bar(1 + wk, 64);
         if (warp == 0) continue;
         if (t == 0) A.strip_tiles[(size_t)b * a.S + s] = nstored;
         if (A.trace && t == 0)
@@ -784,7 +803,7 @@ __global__ void __launch_bounds__(64, 1) sdtw_backward4_kernel(Dp3Args<T> A, uns
     if constexpr (kTc) {
         tc::tc_fence_before();
         __syncthreads();
-        if (warp == 0) tc::tmem_dealloc<128>(tmem);
+        if (threadIdx.x < 32) tc::tmem_dealloc<128 * kW>(tmem_slot);
     }
 }
 
