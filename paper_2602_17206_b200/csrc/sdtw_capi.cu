@@ -431,14 +431,17 @@ struct Pipeline {
             // operands packed once (fp16 hi/lo core-matrix images), then
             // bulk-copied by every CTA that needs them
             const int NB = (N + 127) / 128;
-            Buf<uint8_t> xp(ctx, (size_t)B * NB * 128 * dpad * 4), yp(ctx, (size_t)B * C * 32 * dpad * 4);
+            // y as overlapping 160-row blocks [128 jb - 32, 128 jb + 128): the
+            // B operand of one N = 160 MMA per K step
+            const int JB = (M + 127) / 128;
+            Buf<uint8_t> xp(ctx, (size_t)B * NB * 128 * dpad * 4), yp(ctx, (size_t)B * JB * 160 * dpad * 4);
             LAUNCH(ctx, sdtw::pack_split_kernel, grid_for(xp.n / 64, 256, 8192), 256, 0, x, B, N, D, dpad, 128,
-                   absmax.p, 0, xp.p);
-            LAUNCH(ctx, sdtw::pack_split_kernel, grid_for(yp.n / 64, 256, 8192), 256, 0, y, B, M, D, dpad, 32,
-                   absmax.p, 1, yp.p);
-            dim3 grid((M + 127) / 128, NB, B);
-            LAUNCH(ctx, sdtw::cost_gemm_tc_kernel, grid, 256, sdtw::kCgSmem, xp.p, yp.p, xn.p, yn.p, absmax.p, B,
-                   N, M, S, C, KK, bw, dpad, dsk.p);
+                   absmax.p, 0, xp.p, 0, 0);
+            LAUNCH(ctx, sdtw::pack_split_kernel, grid_for(yp.n / 64, 256, 8192), 256, 0, y, B, M, D, dpad, 160,
+                   absmax.p, 1, yp.p, 128, -32);
+            const int ntiles = B * NB * ((M + 127) / 128);
+            LAUNCH(ctx, sdtw::cost_gemm_tc_kernel, (unsigned)std::min(ntiles, ctx->sm_count), sdtw::kCgThreads,
+                   sdtw::kCgSmem, xp.p, yp.p, xn.p, yn.p, absmax.p, B, N, M, S, C, KK, bw, dpad, dsk.p);
         } else {
             LAUNCH(ctx, sdtw::cost_skewed_kernel<T>, grid_for(total, 256), 256, 0, x, y, xn.p, yn.p, B,
                    N, M, D, S, KK, bw, dsk.p);

@@ -261,6 +261,11 @@ __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__re
     }
 }
 
+__device__ __forceinline__ void named_bar_cg(int id, int threads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 // The cost epilogue shared by all tensor-core paths (the unfused GEMM, the
 // fused forward and the fused backward recompute): accumulator acc of row i,
 // column j; d = ||x_i||^2 + ||y_j||^2 - 2 <x_i, y_j>, clamped at 0
@@ -279,10 +284,14 @@ __device__ __forceinline__ float tc_cost(float acc, float xi, float yj, float m2
 // features >= D zero.  One thread per 16-byte core-matrix row, split exactly
 // as split_store8.  which = 0: x (scale sx), 1: y (scale sy).
 // ----------------------------------------------------------------------------
+// Block k covers rows [k rstride + roff, + rpb) (rstride = rpb, roff = 0 for
+// a plain tiling; the GEMM's B operand uses overlapping 160-row blocks).
 __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, int D, int dpad, int rpb,
-                                  const unsigned *absmax, int which, uint8_t *__restrict__ dst)
+                                  const unsigned *absmax, int which, uint8_t *__restrict__ dst, int rstride = 0,
+                                  int roff = 0)
 {
-    const int nblk = (R + rpb - 1) / rpb;
+    if (rstride == 0) rstride = rpb;
+    const int nblk = (R + rstride - 1) / rstride;  // blocks start at k rstride + roff (roff <= 0)
     const int kbn = dpad / 8;
     const size_t total = (size_t)B * nblk * rpb * kbn;
     const SplitScale sc = split_scale(absmax);
@@ -295,12 +304,12 @@ __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, i
         const size_t bb = rest / kbn;        // b * nblk + blk
         const int blk = (int)(bb % nblk);
         const int b = (int)(bb / nblk);
-        const int row = blk * rpb + r;
+        const int row = blk * rstride + roff + r;
         uint8_t *hi = dst + bb * (size_t)rpb * dpad * 4;
         uint8_t *lo = hi + (size_t)rpb * dpad * 2;
         const int k = kb * 8;
-        const int nk = row < R ? max(0, min(8, D - k)) : 0;
-        const float *p = src + ((size_t)b * R + min(row, R - 1)) * D + min(k, D - 1);
+        const int nk = (row >= 0 && row < R) ? max(0, min(8, D - k)) : 0;
+        const float *p = src + ((size_t)b * R + min(max(row, 0), R - 1)) * D + min(k, D - 1);
         tc::split_store8(p, s, hi, lo, tc::kmajor_off(r, kb, rpb * 16), nk, vec && nk == 8);
     }
 }
@@ -320,148 +329,189 @@ __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, i
 // up to KK.
 // ----------------------------------------------------------------------------
 constexpr int kCgPitch = 162;
-constexpr int kCgSmem = 4 * 32 * kCgPitch * 4;  // 82944 B >= one round's operands (72 KB)
+constexpr int kCgStageBytes = 32768 + 40960;                  // one round's operands: A 32 KB + B 40 KB
+constexpr int kCgEpiBytes = 4 * 32 * kCgPitch * 4;            // epilogue staging (81 KB)
+constexpr int kCgSmem = 2 * kCgStageBytes + kCgEpiBytes;      // 225 KB: two operand stages + staging
+constexpr int kCgThreads = 288;                               // 8 epilogue warps + 1 producer warp
 
-__global__ void __launch_bounds__(256, 1)
+struct CgShared {
+    uint64_t st_full[2], st_empty[2], acc_full[2], acc_empty[2];
+    uint32_t tmem_base;
+};
+
+// Persistent and pipelined: TMEM kernels run one CTA per SM, so each CTA
+// walks tiles (b, ib, jb) with the producer warp loading round g + 1 while
+// the MMAs of round g run, and the eight epilogue warps draining tile n - 1
+// from the other TMEM accumulator (2 x 160 columns) while tile n is computed.
+__global__ void __launch_bounds__(kCgThreads, 1)
     cost_gemm_tc_kernel(const uint8_t *__restrict__ xp, const uint8_t *__restrict__ yp, const float *__restrict__ xn,
                         const float *__restrict__ yn, const unsigned *absmax, int B, int N, int M, int S, int C,
                         int KK, int bw, int dpad, float *__restrict__ dsk)
 {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bars[2];  // [0] operand bytes landed, [1] MMAs done
-    __shared__ uint32_t tmem_base;
+    __shared__ CgShared sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int b = blockIdx.z, ib = blockIdx.y, jb = blockIdx.x;
-    const int i0 = 128 * ib, j0 = 128 * jb;
-    const int NB = (N + 127) / 128;
+    const int NB = (N + 127) / 128, JB = (M + 127) / 128;
+    const int ntiles = B * NB * JB;
+    const int rounds = dpad / 64;
     const SplitScale sc = split_scale(absmax);
-
-    if (warp == 0) tc::tmem_alloc<256>(&tmem_base);
     if (tid == 0) {
-        tc::mbar_init(&bars[0], 1);
-        tc::mbar_init(&bars[1], 1);
+        for (int k = 0; k < 2; ++k) {
+            tc::mbar_init(&sh.st_full[k], 1);
+            tc::mbar_init(&sh.st_empty[k], 1);
+            tc::mbar_init(&sh.acc_full[k], 1);
+            tc::mbar_init(&sh.acc_empty[k], 8);
+        }
         tc::fence_barrier_init();
     }
+    if (warp == 0) tc::tmem_alloc<512>(&sh.tmem_base);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
-    const uint32_t tmem = tmem_base;
+    const uint32_t tmem = sh.tmem_base;
+    auto tile_of = [&](int n, int &b, int &ib, int &jb) {
+        jb = n % JB;
+        const int r = n / JB;
+        ib = r % NB;
+        b = r / NB;
+    };
 
-    const uint8_t *xa = xp + ((size_t)b * NB + ib) * (size_t)128 * dpad * 4;
-    const uint32_t idesc = tc::idesc_f16_f32(128, 32);
-    const int rounds = dpad / 64;
-    int zlo = 0;
-    while (4 * jb - 1 + zlo < 0) ++zlo;  // chunk -1 does not exist
-    int zhi = 5;
-    while (zhi > zlo && 4 * jb - 1 + zhi - 1 >= C) --zhi;
-    for (int kc = 0; kc < rounds; ++kc) {
-        if (tid == 0) {
-            const uint32_t bytes = 32768u + (uint32_t)(zhi - zlo) * 8192u;
-            tc::mbar_expect_tx(&bars[0], bytes);
-            tc::bulk_g2s(smem, xa + (size_t)kc * 16384, 16384, &bars[0]);
-            tc::bulk_g2s(smem + 16384, xa + (size_t)128 * dpad * 2 + (size_t)kc * 16384, 16384, &bars[0]);
-            for (int z = zlo; z < zhi; ++z) {
-                const uint8_t *yb = yp + ((size_t)b * C + (4 * jb - 1 + z)) * (size_t)32 * dpad * 4;
-                tc::bulk_g2s(smem + 32768 + z * 8192, yb + (size_t)kc * 4096, 4096, &bars[0]);
-                tc::bulk_g2s(smem + 32768 + z * 8192 + 4096, yb + (size_t)32 * dpad * 2 + (size_t)kc * 4096, 4096,
-                             &bars[0]);
-            }
-        }
-        tc::mbar_wait(&bars[0], kc & 1);
-        if (tid == 0) {
-            tc::tc_fence_after();
-            const uint32_t ah = tc::smem_u32(smem), al = ah + 16384;
-            for (int z = zlo; z < zhi; ++z) {
-                const uint32_t bh = tc::smem_u32(smem + 32768 + z * 8192), bl = bh + 4096;
-                const uint32_t d = tmem + 32u * z;
-                for (int ks = 0; ks < 4; ++ks) {
-                    const int kg = 4 * kc + ks;
-                    const uint32_t oa = ks * 4096, ob = ks * 1024;
-                    const uint32_t acc0 = kg > 0 ? 1u : 0u;
-                    tc::mma_f16(d, tc::smem_desc(ah + oa, 2048, 128), tc::smem_desc(bh + ob, 512, 128), idesc, acc0);
-                    tc::mma_f16(d, tc::smem_desc(ah + oa, 2048, 128), tc::smem_desc(bl + ob, 512, 128), idesc, 1u);
-                    tc::mma_f16(d, tc::smem_desc(al + oa, 2048, 128), tc::smem_desc(bh + ob, 512, 128), idesc, 1u);
+    if (warp == 8) {
+        // ---------------------------------------------------------------- producer
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_f16_f32(128, 160);
+            int g = 0;  // global round counter of this CTA
+            auto issue_load = [&](int n, int kc, int gg) {
+                int b, ib, jb;
+                tile_of(n, b, ib, jb);
+                const int sb = gg & 1;
+                uint8_t *st = smem + sb * kCgStageBytes;
+                tc::mbar_wait(&sh.st_empty[sb], ((gg >> 1) & 1) ^ 1);
+                const uint8_t *xa = xp + ((size_t)b * NB + ib) * (size_t)128 * dpad * 4;
+                const uint8_t *ya = yp + ((size_t)b * JB + jb) * (size_t)160 * dpad * 4;
+                tc::mbar_expect_tx(&sh.st_full[sb], 32768u + 40960u);
+                tc::bulk_g2s(st, xa + (size_t)kc * 16384, 16384, &sh.st_full[sb]);
+                tc::bulk_g2s(st + 16384, xa + (size_t)128 * dpad * 2 + (size_t)kc * 16384, 16384, &sh.st_full[sb]);
+                tc::bulk_g2s(st + 32768, ya + (size_t)kc * 20480, 20480, &sh.st_full[sb]);
+                tc::bulk_g2s(st + 32768 + 20480, ya + (size_t)160 * dpad * 2 + (size_t)kc * 20480, 20480,
+                             &sh.st_full[sb]);
+            };
+            int li = 0;  // local tile index
+            const int first = blockIdx.x;
+            if (first < ntiles) issue_load(first, 0, 0);
+            for (int n = first; n < ntiles; n += gridDim.x, ++li) {
+                const int ab = li & 1;
+                tc::mbar_wait(&sh.acc_empty[ab], ((li >> 1) & 1) ^ 1);  // epilogue done with tile li - 2
+                tc::tc_fence_after();
+                for (int kc = 0; kc < rounds; ++kc, ++g) {
+                    // prefetch the next round (this tile's or the next tile's first)
+                    if (kc + 1 < rounds) issue_load(n, kc + 1, g + 1);
+                    else if (n + (int)gridDim.x < ntiles) issue_load(n + gridDim.x, 0, g + 1);
+                    const int sb = g & 1;
+                    tc::mbar_wait(&sh.st_full[sb], (g >> 1) & 1);
+                    tc::tc_fence_after();
+                    // one M = 128, N = 160 MMA per K step and pass: B = the
+                    // 160 y rows [j0 - 32, j0 + 128) (K-block stride 2560 B)
+                    const uint32_t ah = tc::smem_u32(smem + sb * kCgStageBytes), al = ah + 16384;
+                    const uint32_t bh = ah + 32768, bl = bh + 20480;
+                    const uint32_t d = tmem + 256u * ab;
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const int kg = 4 * kc + ks;
+                        const uint32_t oa = ks * 4096, ob = ks * 5120;
+                        const uint32_t acc0 = kg > 0 ? 1u : 0u;
+                        tc::mma_f16(d, tc::smem_desc(ah + oa, 2048, 128), tc::smem_desc(bh + ob, 2560, 128), idesc, acc0);
+                        tc::mma_f16(d, tc::smem_desc(ah + oa, 2048, 128), tc::smem_desc(bl + ob, 2560, 128), idesc, 1u);
+                        tc::mma_f16(d, tc::smem_desc(al + oa, 2048, 128), tc::smem_desc(bh + ob, 2560, 128), idesc, 1u);
+                    }
+                    tc::mma_commit(&sh.st_empty[sb]);  // the stage is free once these MMAs finish
                 }
+                tc::mma_commit(&sh.acc_full[ab]);
             }
-            tc::mma_commit(&bars[1]);
         }
         __syncwarp();
-        tc::mbar_wait(&bars[1], kc & 1);  // the next round overwrites the operands
-        tc::tc_fence_after();
-    }
-
-    // epilogue: warp w reads TMEM lane quarter q = w & 3 (rows i0 + 32 q +
-    // lane); warps 0-3 take chunks z = 0..2, warps 4-7 chunks 3..4
-    const int q = warp & 3, hf = warp >> 2;
-    float *stage = reinterpret_cast<float *>(smem) + q * 32 * kCgPitch;
-    const int i = i0 + 32 * q + lane;
-    const bool row_ok = i < N;
-    const float xi = row_ok ? xn[(size_t)b * N + i] : 0.f;
-    const float m2 = -2.0f * sc.inv;
-    const int zb = hf == 0 ? 0 : 3, ze = hf == 0 ? 3 : 5;
-    float yv[3];
+    } else {
+        // ---------------------------------------------------------------- epilogue
+        // warp w reads TMEM lane quarter q = w & 3 (rows i0 + 32 q + lane);
+        // warps 0-3 take chunks z = 0..2, warps 4-7 chunks 3..4
+        const int q = warp & 3, hf = warp >> 2;
+        float *stage = reinterpret_cast<float *>(smem + 2 * kCgStageBytes) + q * 32 * kCgPitch;
+        const float m2 = -2.0f * sc.inv;
+        const int zb = hf == 0 ? 0 : 3, ze = hf == 0 ? 3 : 5;
+        int li = 0;
+        for (int n = blockIdx.x; n < ntiles; n += gridDim.x, ++li) {
+            int b, ib, jb;
+            tile_of(n, b, ib, jb);
+            const int i0 = 128 * ib, j0 = 128 * jb;
+            const int ab = li & 1;
+            const int i = i0 + 32 * q + lane;
+            const bool row_ok = i < N;
+            const float xi = row_ok ? xn[(size_t)b * N + i] : 0.f;
+            float yv[3];
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-        const int j = j0 - 32 + 32 * (zb + u) + lane;
-        yv[u] = (zb + u < ze && j >= 0 && j < M) ? yn[(size_t)b * M + j] : 0.f;
-    }
-    __syncthreads();  // all MMAs done and read: the operand area becomes the stage
-    // interior block: every column in [0, M), no band, all rows valid
-    const bool interior = j0 >= 32 && j0 + 128 <= M && bw == 0 && i0 + 128 <= N;
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-        const int z = zb + u;
-        if (z >= ze) break;
-        float acc[32];
-        if (z >= zlo && z < zhi) {
-            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * z), acc);
-        } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) acc[e] = 0.f;
-        }
-        const int jz = j0 - 32 + 32 * z;
-        float *st = stage + lane * kCgPitch + 32 * z;
-        if (interior) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) st[e] = tc_cost(acc[e], xi, __shfl_sync(kFull, yv[u], e), m2, true);
-        } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                const float yj = __shfl_sync(kFull, yv[u], e);
-                const int j = jz + e;
-                const bool ok = row_ok && j >= 0 && j < M && in_band(i + 1, j + 1, bw);
-                st[e] = tc_cost(acc[e], xi, yj, m2, ok);
+            for (int u = 0; u < 3; ++u) {
+                const int j = j0 - 32 + 32 * (zb + u) + lane;
+                yv[u] = (zb + u < ze && j >= 0 && j < M) ? yn[(size_t)b * M + j] : 0.f;
             }
-        }
-    }
-    __syncthreads();
-    const int s = 4 * ib + q;
-    if (32 * s < N) {
-        float *ds = dsk + ((size_t)b * S + s) * (size_t)KK * 32;
-        const bool last = jb == (M + 127) / 128 - 1;
-        const int rend = last ? KK : min(j0 + 128, KK);
-        const int t4 = 4 * (lane & 7);
-        // the two warps of a lane quarter take alternate groups of 4 rows
-        for (int kk0 = j0 + 4 * hf; kk0 < rend; kk0 += 8) {
-            const int kk = kk0 + (lane >> 3);
-            const float *sr = stage + kk - j0 + 32;  // + t * (pitch - 1) - ... below
-            float v[4];
-            if (!last) {
+            tc::mbar_wait(&sh.acc_full[ab], (li >> 1) & 1);
+            tc::tc_fence_after();
+            // the staging area is free once every epilogue warp finished the previous tile
+            named_bar_cg(1, 256);
+            const bool interior = j0 >= 32 && j0 + 128 <= M && bw == 0 && i0 + 128 <= N;
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) v[c4] = sr[(t4 + c4) * (kCgPitch - 1)];
-            } else {
+            for (int u = 0; u < 3; ++u) {
+                const int z = zb + u;
+                if (z >= ze) break;
+                float acc[32];
+                tc::tmem_ld32(tmem + 256u * ab + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * z), acc);
+                const int jz = j0 - 32 + 32 * z;
+                float *st = stage + lane * kCgPitch + 32 * z;
+                if (interior) {
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    const int lc = kk - (t4 + c4) - j0 + 32;  // local column of lane t4 + c4
-                    v[c4] = lc < 160 ? stage[(t4 + c4) * kCgPitch + lc] : 0.f;
+                    for (int e = 0; e < 32; ++e) st[e] = tc_cost(acc[e], xi, __shfl_sync(kFull, yv[u], e), m2, true);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float yj = __shfl_sync(kFull, yv[u], e);
+                        const int j = jz + e;
+                        const bool ok = row_ok && j >= 0 && j < M && in_band(i + 1, j + 1, bw);
+                        st[e] = tc_cost(acc[e], xi, yj, m2, ok);
+                    }
                 }
             }
-            *reinterpret_cast<float4 *>(ds + (size_t)kk * 32 + t4) = make_float4(v[0], v[1], v[2], v[3]);
+            // this warp's TMEM reads are complete: release the accumulator
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sh.acc_empty[ab]);
+            named_bar_cg(1, 256);
+            const int s = 4 * ib + q;
+            if (32 * s < N) {
+                float *ds = dsk + ((size_t)b * S + s) * (size_t)KK * 32;
+                const bool last = jb == JB - 1;
+                const int rend = last ? KK : min(j0 + 128, KK);
+                const int t4 = 4 * (lane & 7);
+                // the two warps of a lane quarter take alternate groups of 4 rows
+                for (int kk0 = j0 + 4 * hf; kk0 < rend; kk0 += 8) {
+                    const int kk = kk0 + (lane >> 3);
+                    const float *sr = stage + kk - j0 + 32;
+                    float v[4];
+                    if (!last) {
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) v[c4] = sr[(t4 + c4) * (kCgPitch - 1)];
+                    } else {
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            const int lc = kk - (t4 + c4) - j0 + 32;
+                            v[c4] = lc < 160 ? stage[(t4 + c4) * kCgPitch + lc] : 0.f;
+                        }
+                    }
+                    *reinterpret_cast<float4 *>(ds + (size_t)kk * 32 + t4) = make_float4(v[0], v[1], v[2], v[3]);
+                }
+            }
         }
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<256>(tmem);
+    if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace sdtw
