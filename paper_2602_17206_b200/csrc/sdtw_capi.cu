@@ -357,6 +357,11 @@ struct Pipeline {
         KK = ((M + 62) / 32) * 32;
         dpad = ((D + 63) / 64) * 64;
         tc_fused = fused && std::is_same<T, float>::value && dpad <= sdtw::kFtcMaxD;
+        // fp32 with D > 128: the fused tensor-core kernels stage at most 128
+        // features per operand row, so the call runs the unfused schedule
+        // (tensor-core cost tensor; identical costs, the tensor is
+        // materialised).  fp64 fused mode keeps per-cell SIMT costs.
+        if (fused && std::is_same<T, float>::value && !tc_fused) fused = false;
     }
 
     // fp32 fused mode with D <= 128 runs on the tensor cores (sdtw_fused.cuh);
