@@ -114,6 +114,9 @@ int sdtw_fwd_bwd_f64(sdtw_ctx *ctx, const double *x, const double *y,
 /* ---- forward (forward.hpp:43-81) ----------------------------------------
  * loss: B.  R_out (nullable): the padded accumulated-cost table
  * B*(N+2)*(M+2) with the reference's +inf boundary and R[b,0,0] = 0.
+ * cfg->normalized = 1: forward_normalized (forward.hpp:85-102), loss =
+ *   sdtw(x,y) - (sdtw(x,x) + sdtw(y,y)) / 2 (requires N == M; R_out /
+ *   costs_out / norms_out then describe the (x, y) pass).
  * costs_out (nullable): the B*N*M cost tensor (unfused mode only).
  * norms_out (nullable): B*N then B*M squared norms (NormCache, cost.hpp:12-20). */
 int sdtw_forward_f32(sdtw_ctx *ctx, const float *x, const float *y, size_t B,

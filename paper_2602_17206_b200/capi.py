@@ -256,9 +256,9 @@ class Engine:
         self.lib.sdtw_reset_launch_count(self.ctx)
 
     @staticmethod
-    def _cfg(gamma, bandwidth, fused, linear):
+    def _cfg(gamma, bandwidth, fused, linear, normalized=False):
         return sdtw_config(float(gamma), int(bandwidth), COST_FUSED if fused else COST_UNFUSED,
-                           BWD_LINEAR if linear else BWD_LOG, 0)
+                           BWD_LINEAR if linear else BWD_LOG, 1 if normalized else 0)
 
     @staticmethod
     def _suffix(dtype):
@@ -304,7 +304,7 @@ class Engine:
 
     # ---- forward (forward.hpp:43-81) ------------------------------------
     def forward(self, x, y, gamma=1.0, bandwidth=0, fused=False, dtype=np.float64, table=False,
-                costs=False, norms=False):
+                costs=False, norms=False, normalized=False):
         B, N, M, D = self._dims(x, y)
         a = _Args(dtype)
         px, py = a.inp(x), a.inp(y)
@@ -312,7 +312,7 @@ class Engine:
         R = self._alloc_like(x, (B, N + 2, M + 2), dtype) if table else None
         dc = self._alloc_like(x, (B, N, M), dtype) if costs else None
         nm = self._alloc_like(x, (B * (N + M),), dtype) if norms else None
-        cfg = self._cfg(gamma, bandwidth, fused, False)
+        cfg = self._cfg(gamma, bandwidth, fused, False, normalized)
         fn = getattr(self.lib, f"sdtw_forward_{self._suffix(dtype)}")
         _raise(fn(self.ctx, px, py, B, N, M, D, C.byref(cfg), a.kind, a.out(loss), a.out(R),
                   a.out(dc), a.out(nm)))

@@ -333,4 +333,12 @@ __global__ void adam_kernel(T *__restrict__ z, const T *__restrict__ g, double *
     z[i] -= (T)step;
 }
 
+// forward_normalized (forward.hpp:97-100): loss[b] = xy[b] - (xx[b] + yy[b]) / 2, in T.
+template <class T>
+__global__ void normalize_loss_kernel(const T *__restrict__ xx, const T *__restrict__ yy, int B, T *__restrict__ xy)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) xy[b] = xy[b] - (xx[b] + yy[b]) / T(2);
+}
+
 }  // namespace sdtw

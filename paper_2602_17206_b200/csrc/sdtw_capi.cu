@@ -800,6 +800,25 @@ int forward_api(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_
         pl.norms();
         pl.costs();
         loss_out<T>(pl, ldev);
+        if (cfg->normalized) {
+            // forward_normalized (forward.hpp:85-102): sdtw(x,y) - (sdtw(x,x) + sdtw(y,y)) / 2
+            sdtw_config plain = *cfg;
+            plain.normalized = 0;
+            Buf<T> lxx(ctx, B), lyy(ctx, B);
+            {
+                Pipeline<T> px(ctx, xi.p, xi.p, B, N, N, D, &plain);
+                px.norms();
+                px.costs();
+                loss_out<T>(px, lxx.p);
+            }
+            {
+                Pipeline<T> py(ctx, yi.p, yi.p, B, M, M, D, &plain);
+                py.norms();
+                py.costs();
+                loss_out<T>(py, lyy.p);
+            }
+            LAUNCH(ctx, sdtw::normalize_loss_kernel<T>, grid_for(B, 128), 128, 0, lxx.p, lyy.p, (int)B, ldev);
+        }
         if (no.p) {
             CUDA_OK(cudaMemcpyAsync(no.p, pl.xn.p, B * N * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
             CUDA_OK(cudaMemcpyAsync(no.p + B * N, pl.yn.p, B * M * sizeof(T), cudaMemcpyDeviceToDevice,

@@ -278,3 +278,21 @@ def test_tile_store_overflow_path(engine, oracle_c, monkeypatch):
     assert rel_err(a[0], ref[0]).max() <= F32_LOSS
     for g, r in zip(a[1:], ref[1:]):
         assert grad_stats(g, r)[0] <= F32_GRAD_MAX
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_forward_normalized(engine, oracle_c, fused):
+    """forward_normalized (forward.hpp:85-102): sdtw(x,y) - (sdtw(x,x) + sdtw(y,y)) / 2,
+    exactly 0 when x == y."""
+    rng = np.random.default_rng(77)
+    x = rng.uniform(-1, 1, (3, 40, 5)); y = rng.uniform(-1, 1, (3, 40, 5))
+    ref = []
+    for a_, b_ in ((x, y), (x, x), (y, y)):
+        ref.append(oracle_c.sdtw_with_gradients(a_, b_, 0.5)[1])
+    want = ref[0] - (ref[1] + ref[2]) / 2
+    got = engine.forward(x, y, 0.5, fused=fused, dtype=np.float64, normalized=True)[0]
+    assert rel_err(got, want).max() <= F64_LOSS
+    same = engine.forward(x, x, 0.5, fused=fused, dtype=np.float64, normalized=True)[0]
+    assert np.abs(same).max() <= 1e-9
+    with pytest.raises(Exception):
+        engine.forward(x, y[:, :30], 0.5, dtype=np.float64, normalized=True)
