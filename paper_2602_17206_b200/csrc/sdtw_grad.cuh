@@ -140,24 +140,44 @@ __global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restri
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc[a][q] = T(0);
             double marg[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int e = lo; e < hi; ++e) {
+            // tile operands go through registers one tile ahead: the loads of
+            // tile e + 1 are in flight while tile e is contracted
+            T re[4], rp[16];
+            int np_next = 0;
+            auto load_tile = [&](int e) {
                 const int idx = which == 0 ? e : ord[e];
                 const int4 m = meta[idx];
                 const T *et = tiles + (size_t)idx * 1024;  // [r][jj]
                 const int p0 = which == 0 ? 32 * m.z : 32 * m.y;
                 const int np = which == 0 ? m.w : min(32, N - 32 * m.y);
-                __syncthreads();
-                for (int u = tid; u < 1024; u += 256) {
-                    const int r = u >> 5, jj = u & 31;
-                    const T v = et[u];
-                    if (which == 0) Et[jj][r] = v;  // o = r, m = jj
-                    else Et[r][jj] = v;             // o = jj, m = r
-                }
-                for (int u = tid; u < 32 * 128; u += 256) {
+                np_next = np;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) re[q] = et[tid + 256 * q];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int u = tid + 256 * q;
                     const int r = u >> 7, k = u & 127;
-                    P[r][k] = (r < np && kb + k < D) ? vp[(size_t)(p0 + r) * D + kb + k] : T(0);
+                    rp[q] = (r < np && kb + k < D) ? vp[(size_t)(p0 + r) * D + kb + k] : T(0);
+                }
+            };
+            if (lo < hi) load_tile(lo);
+            for (int e = lo; e < hi; ++e) {
+                const int np = np_next;
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int u = tid + 256 * q;
+                    const int r = u >> 5, jj = u & 31;
+                    if (which == 0) Et[jj][r] = re[q];  // o = r, m = jj
+                    else Et[r][jj] = re[q];             // o = jj, m = r
+                }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int u = tid + 256 * q;
+                    P[u >> 7][u & 127] = rp[q];
                 }
                 __syncthreads();
+                if (e + 1 < hi) load_tile(e + 1);
                 for (int mm = 0; mm < np; ++mm) {
                     T ev[4], pv[4];
                     if constexpr (sizeof(T) == 4) {
