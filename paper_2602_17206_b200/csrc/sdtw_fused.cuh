@@ -127,15 +127,6 @@ struct FusedTcArgs {
     int dpad;  // D rounded up to 64 (<= kFtcMaxD): the unfused GEMM's K padding
 };
 
-#ifndef FTC_EXP_NO_MMA
-#define FTC_EXP_NO_MMA 0  // experiment builds only: skip the cost MMAs
-#endif
-#ifndef FTC_EXP_NO_STG
-#define FTC_EXP_NO_STG 0  // experiment builds only: skip the L2 halo stores
-#endif
-#ifndef FTC_EXP_NO_HX
-#define FTC_EXP_NO_HX 0   // experiment builds only: skip the shared hand-off stores
-#endif
 constexpr int kFtcMaxD = 128;
 constexpr int kFtcRing = 8;       // TMEM cost tiles per slot (128 lanes x 32 columns)
 constexpr int kFtcHx = 32;        // intra-slot h hand-off ring (columns)
@@ -404,12 +395,10 @@ for (int k8 = 0; k8 < 32; k8 += 8) {
             vck = (kl == ((t - 1) & 31)) ? v : vck;
             l_carry = v;
             h_prev = h;
-            if (!FTC_EXP_NO_STG) TG::store_if(hb_me + col, h, epoch, t == 31 && active);
+            TG::store_if(hb_me + col, h, epoch, t == 31 && active);
             const unsigned pos = base + (unsigned)col;
-            if (!FTC_EXP_NO_HX)
-                st_shared_u64_if(hx_me + (pos & (kFtcHx - 1)),
-                                 ((unsigned long long)pos << 32) | __float_as_uint(h),
-                                 pub_local && t == 31 && active);
+            st_shared_u64_if(hx_me + (pos & (kFtcHx - 1)), ((unsigned long long)pos << 32) | __float_as_uint(h),
+                             pub_local && t == 31 && active);
         }
     };
     if (fixup || tail) steps8(std::true_type{});
@@ -446,7 +435,6 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
     const int dpad = F.dpad;
     const int SSn = (a.S + 3) / 4;
     const int total = a.B * SSn;
-    const unsigned epoch = A.epoch;
     const unsigned Mu = (unsigned)a.M;
 
     if (threadIdx.x == 0) {
@@ -514,7 +502,7 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
                 if (leader) {
                     tc::mbar_wait(&sh.empty[p][sl], ((u / kFtcRing) & 1) ^ 1);
                     tc::tc_fence_after();
-                    if (t == 0 && !FTC_EXP_NO_MMA) {
+                    if (t == 0) {
                         const uint32_t d = tmem + 256u * p + 32u * sl;
                         const uint32_t ah = tc::smem_u32(xs), al = ah + 128u * dpad * 2;
                         const uint32_t bh = tc::smem_u32(ys), bl = bh + 32u * dpad * 2;
@@ -527,7 +515,6 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
                         }
                         tc::mma_commit(&sh.full[p][sl]);
                     }
-                    if (t == 0 && FTC_EXP_NO_MMA) tc::mbar_arrive(&sh.full[p][sl]);
                     __syncwarp();
                 }
                 // the Y buffer (and, after the last chunk, X) is free once the MMAs finished
