@@ -49,9 +49,38 @@ __device__ __forceinline__ float tmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double tmin(double a, double b) { return fmin(a, b); }
 __device__ __forceinline__ double tmax(double a, double b) { return fmax(a, b); }
 
+// Three-input min / max (FMNMX3, sm_100): min3(u, l, 0), max3(u, l, 0) and
+// the median min3(max(u, l), max(u, 0), max(l, 0)) are the exact values of
+// the two-input sorting network below, two levels shallower on the chain.
+__device__ __forceinline__ float min3f(float a, float b, float c)
+{
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c)
+{
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 template <class T>
 __device__ __forceinline__ void fwd_cell(T d, T u, T l, T k, T gln2, T &g, T &v, T &h)
 {
+    if constexpr (sizeof(T) == 4) {
+        const float mn = min3f(u, l, 0.f);
+        const float mx = max3f(u, l, 0.f);
+        const float md = min3f(fmaxf(u, l), fmaxf(u, 0.f), fmaxf(l, 0.f));
+        const float e1 = Num<float>::ex2((mn - md) * k);
+        const float e2 = Num<float>::ex2((mn - mx) * k);
+        const float s = (e1 + e2) + 1.f;
+        const float sm = mn - gln2 * Num<float>::lg2(s);
+        g = d + sm;
+        v = (d - u) + sm;
+        h = (d - l) + sm;
+        return;
+    }
     const T lo = tmin(u, l);
     const T hi = tmax(u, l);
     const T mn = tmin(lo, T(0));
