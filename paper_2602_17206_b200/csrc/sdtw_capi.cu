@@ -153,6 +153,12 @@ struct sdtw_ctx {
     unsigned long long *trace = nullptr;  // debug: per-strip forward timestamps
     cudaEvent_t ev[SDTW_NUM_PHASES][2] = {};
     bool ev_used[SDTW_NUM_PHASES] = {};
+    // Host-pointer calls split the batch into pair chunks, each on its own
+    // sub-context (stream, stream-ordered allocator, halo arena), so the
+    // host<->device copies of one chunk overlap the DP of the others.
+    std::vector<sdtw_ctx *> subs;
+    cudaEvent_t fork_ev = nullptr;
+    std::vector<cudaEvent_t> join_ev;
 };
 
 namespace {
@@ -720,6 +726,66 @@ void check_finite_loss(sdtw_ctx *ctx, const T *loss_dev, size_t B)
             fail(SDTW_EUNREACHABLE, "forward: R[N,M] is not finite (end cell unreachable)");
 }
 
+// One chunk of pairs through the whole pipeline on `c`'s stream (host or
+// device pointers already offset to the chunk).
+template <class T>
+void fwd_bwd_run(sdtw_ctx *c, const T *x, const T *y, size_t B, size_t N, size_t M, size_t D,
+                 const sdtw_config *cfg, bool host, T *loss, T *gx, T *gy)
+{
+    In<T> xi(c, x, B * N * D, host), yi(c, y, B * M * D, host);
+    Out<T> lo(c, loss, B, host), gxo(c, gx, B * N * D, host), gyo(c, gy, B * M * D, host);
+    Pipeline<T> pl(c, xi.p, yi.p, B, N, M, D, cfg);
+    pl.norms();
+    pl.costs();
+    loss_out<T>(pl, lo.p);
+    pl.backward(gxo.p, gyo.p, false);
+    lo.finish(c);
+    gxo.finish(c);
+    gyo.finish(c);
+}
+
+sdtw_ctx *sub_context(sdtw_ctx *ctx, size_t i)
+{
+    while (ctx->subs.size() <= i) {
+        auto *c = new sdtw_ctx();
+        c->device = ctx->device;
+        c->sm_count = ctx->sm_count;
+        if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            fail(SDTW_ECUDA, "cudaStreamCreate failed (sub-context)");
+        }
+        c->stream = c->own_stream;
+        ctx->subs.push_back(c);
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->join_ev.push_back(e);
+    }
+    if (!ctx->fork_ev) CUDA_OK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+    return ctx->subs[i];
+}
+
+// Number of pair chunks for a host-pointer fwd+bwd call: the copies of a
+// B=32, L=1024, D=128 call take ~1.2 ms over PCIe against ~1 ms of device
+// work, so overlapping them is worth up to 2x end to end.  Off for device
+// pointers, asynchronous calls, a ledger limit (one allocator keeps the
+// limit exact), phase timing, and tiny batches.
+size_t e2e_chunks(sdtw_ctx *ctx, size_t B, size_t N, size_t M, size_t D, int ptr_kind)
+{
+    if ((ptr_kind & 0xff) != SDTW_PTR_HOST || (ptr_kind & SDTW_FLAG_ASYNC)) return 1;
+    if (ctx->alloc.limit_bytes != 0 || ctx->timing || ctx->trace) return 1;
+    if (const char *e = std::getenv("SDTW_E2E_CHUNKS"))  // explicit (tests, experiments)
+        return std::min<size_t>(B, std::max<size_t>(1, std::strtoull(e, nullptr, 10)));
+    // below ~8 MB of inputs the copies are shorter than a kernel launch train
+    if ((N + M) * D * B * 4 < ((size_t)8 << 20)) return 1;
+    // the overlap pays when the DP is latency-bound (few strips per SM: a
+    // chunk of B/4 pairs then takes nearly the time of the whole batch);
+    // with many strips (C3) the chunks' kernels only contend for the SMs
+    // (measured, scripts/e2e_timeline.py: C2 2.26 -> 2.02 ms, C3 no gain)
+    const size_t strips = B * ((N + 31) / 32);
+    if (strips > (size_t)ctx->sm_count * 8) return 1;
+    return std::min<size_t>(4, B);
+}
+
 template <class T>
 int fwd_bwd(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_t M, size_t D,
             const sdtw_config *cfg, int ptr_kind, T *loss, T *gx, T *gy)
@@ -728,19 +794,33 @@ int fwd_bwd(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_t M,
         validate(B, N, M, D, cfg);
         if (!loss) fail(SDTW_EINVAL, "loss output is required");
         const bool host = (ptr_kind & 0xff) == SDTW_PTR_HOST;
-        In<T> xi(ctx, x, B * N * D, host), yi(ctx, y, B * M * D, host);
-        Out<T> lo(ctx, loss, B, host), gxo(ctx, gx, B * N * D, host), gyo(ctx, gy, B * M * D, host);
         if (cfg->backward_space == SDTW_BWD_LINEAR) {
             fail(SDTW_EINVAL, "linear-space backward is served by sdtw_backward_table_*");
         }
-        Pipeline<T> pl(ctx, xi.p, yi.p, B, N, M, D, cfg);
-        pl.norms();
-        pl.costs();
-        loss_out<T>(pl, lo.p);
-        pl.backward(gxo.p, gyo.p, false);
-        lo.finish(ctx);
-        gxo.finish(ctx);
-        gyo.finish(ctx);
+        const size_t P = e2e_chunks(ctx, B, N, M, D, ptr_kind);
+        if (P > 1) {
+            // fork: every chunk stream starts after the work already queued on ctx->stream
+            for (size_t c = 0; c < P; ++c) sub_context(ctx, c);
+            CUDA_OK(cudaEventRecord(ctx->fork_ev, ctx->stream));
+            size_t peak_extra = 0;
+            for (size_t c = 0; c < P; ++c) {
+                sdtw_ctx *sc = ctx->subs[c];
+                const size_t b0 = B * c / P, b1 = B * (c + 1) / P;
+                CUDA_OK(cudaStreamWaitEvent(sc->stream, ctx->fork_ev, 0));
+                sc->alloc.peak_bytes = sc->alloc.live_bytes;
+                fwd_bwd_run<T>(sc, x + b0 * N * D, y + b0 * M * D, b1 - b0, N, M, D, cfg, true, loss + b0,
+                               gx ? gx + b0 * N * D : nullptr, gy ? gy + b0 * M * D : nullptr);
+                CUDA_OK(cudaEventRecord(ctx->join_ev[c], sc->stream));
+                CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[c], 0));
+                peak_extra += sc->alloc.peak_bytes;
+                ctx->launches += sc->launches;
+                sc->launches = 0;
+            }
+            ctx->alloc.peak_bytes = std::max(ctx->alloc.peak_bytes, ctx->alloc.live_bytes + peak_extra);
+            finish_call(ctx, ptr_kind);
+            return;
+        }
+        fwd_bwd_run<T>(ctx, x, y, B, N, M, D, cfg, host, loss, gx, gy);
         finish_call(ctx, ptr_kind);
     });
 }
@@ -1052,6 +1132,16 @@ int sdtw_ctx_destroy(sdtw_ctx *ctx)
         DeviceGuard dg(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->nccl_comm && g_nccl.destroy) ((int (*)(void *))g_nccl.destroy)(ctx->nccl_comm);
+        for (auto *sc : ctx->subs) {
+            cudaStreamSynchronize(sc->stream);
+            for (auto &kv : sc->alloc.live) cudaFree(kv.first);
+            if (sc->halo_arena) cudaFree(sc->halo_arena);
+            sc->alloc.trim();
+            if (sc->own_stream) cudaStreamDestroy(sc->own_stream);
+            delete sc;
+        }
+        for (auto e : ctx->join_ev) cudaEventDestroy(e);
+        if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
         for (auto &kv : ctx->alloc.live) cudaFree(kv.first);
         if (ctx->halo_arena) cudaFree(ctx->halo_arena);
         ctx->alloc.trim();
@@ -1102,6 +1192,10 @@ int sdtw_mem_trim(sdtw_ctx *ctx)
     return guarded(ctx, [&] {
         CUDA_OK(cudaStreamSynchronize(ctx->stream));
         ctx->alloc.trim();
+        for (auto *sc : ctx->subs) {
+            CUDA_OK(cudaStreamSynchronize(sc->stream));
+            sc->alloc.trim();
+        }
     });
 }
 

@@ -296,3 +296,28 @@ def test_forward_normalized(engine, oracle_c, fused):
     assert np.abs(same).max() <= 1e-9
     with pytest.raises(Exception):
         engine.forward(x, y[:, :30], 0.5, dtype=np.float64, normalized=True)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_host_call_pair_chunks(engine, oracle_c, monkeypatch, fused, dtype):
+    """Host-pointer calls split the pairs over sub-context streams so copies
+    overlap compute (sdtw_capi.cu e2e_chunks): the chunked call (ragged
+    chunks: 5 pairs over 3 streams) matches the one-stream call and the fp64
+    oracle, and repeated chunked calls are bit-identical."""
+    x, y = _bench_like(5, 150, 24, seed=33)
+    x, y = np.ascontiguousarray(x[:, :137], dtype), np.ascontiguousarray(y, dtype)
+    _, rl, rgx, rgy = oracle_c.sdtw_with_gradients(x.astype(np.float64), y.astype(np.float64), 0.1)
+    monkeypatch.setenv("SDTW_E2E_CHUNKS", "1")
+    one = engine.sdtw_with_gradients(x, y, 0.1, fused=fused, dtype=dtype)
+    monkeypatch.setenv("SDTW_E2E_CHUNKS", "3")
+    a = engine.sdtw_with_gradients(x, y, 0.1, fused=fused, dtype=dtype)
+    b = engine.sdtw_with_gradients(x, y, 0.1, fused=fused, dtype=dtype)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+    lt, gt = (F32_LOSS, F32_GRAD_MAX) if dtype == np.float32 else (F64_LOSS, F64_GRAD)
+    for u, v in zip(a, one):
+        assert rel_err(u, v).max() <= lt
+    assert rel_err(a[0], rl).max() <= lt
+    for g, r in zip(a[1:], (rgx, rgy)):
+        assert grad_stats(g, r)[0] <= gt
