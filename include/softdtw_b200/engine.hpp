@@ -129,6 +129,86 @@ class Context {
         return {value, std::move(grad)};
     }
 
+    // forward (forward.hpp:43-81): loss and, on request, the padded R table
+    // B x (N+2) x (M+2), the cost tensor B x N x M (unfused mode) and the
+    // norm cache (B*N x-norms then B*M y-norms).  cfg.normalized selects
+    // forward_normalized (forward.hpp:85-102).
+    template <class T>
+    struct ForwardOut {
+        std::vector<T> loss, R, costs, norms;
+    };
+    template <class T>
+    ForwardOut<T> forward(const std::vector<T> &x, const std::vector<T> &y, std::size_t B, std::size_t N,
+                          std::size_t M, std::size_t D, const Config &cfg, bool table, bool costs, bool norms)
+    {
+        if (x.size() != B * N * D || y.size() != B * M * D) throw ValidationError("buffer size mismatch");
+        ForwardOut<T> o;
+        o.loss.resize(B);
+        if (table) o.R.resize(B * (N + 2) * (M + 2));
+        if (costs) o.costs.resize(B * N * M);
+        if (norms) o.norms.resize(B * (N + M));
+        const sdtw_config c = cfg.c();
+        T *r = table ? o.R.data() : nullptr, *d = costs ? o.costs.data() : nullptr,
+          *nm = norms ? o.norms.data() : nullptr;
+        if constexpr (sizeof(T) == 4)
+            check(sdtw_forward_f32(ctx_, x.data(), y.data(), B, N, M, D, &c, SDTW_PTR_HOST, o.loss.data(), r, d, nm));
+        else
+            check(sdtw_forward_f64(ctx_, x.data(), y.data(), B, N, M, D, &c, SDTW_PTR_HOST, o.loss.data(), r, d, nm));
+        return o;
+    }
+
+    // backward_log / backward_linear over a padded R table (backward.hpp:183-203).
+    // costs: B x N x M (MaterializedCosts) or null with x / y (FusedCosts).
+    // Returns the linear-space E table, B x (N+2) x (M+2).
+    template <class T>
+    void backward_table(const T *R, const T *costs, const T *x, const T *y, std::size_t B, std::size_t N,
+                        std::size_t M, std::size_t D, const Config &cfg, T *E_out)
+    {
+        const sdtw_config c = cfg.c();
+        if constexpr (sizeof(T) == 4)
+            check(sdtw_backward_table_f32(ctx_, R, costs, x, y, B, N, M, D, &c, SDTW_PTR_HOST, E_out));
+        else
+            check(sdtw_backward_table_f64(ctx_, R, costs, x, y, B, N, M, D, &c, SDTW_PTR_HOST, E_out));
+    }
+
+    // input_gradients (backward.hpp:208-266) from a padded linear E table.
+    template <class T>
+    void input_grads(const T *E, const T *x, const T *y, std::size_t B, std::size_t N, std::size_t M,
+                     std::size_t D, T *gx, T *gy)
+    {
+        if constexpr (sizeof(T) == 4)
+            check(sdtw_input_grads_f32(ctx_, E, x, y, B, N, M, D, SDTW_PTR_HOST, gx, gy));
+        else
+            check(sdtw_input_grads_f64(ctx_, E, x, y, B, N, M, D, SDTW_PTR_HOST, gx, gy));
+    }
+
+    // barycenter_objective for either precision (members K x L x D, equal L).
+    template <class T>
+    double barycenter_objective_into(const T *z, std::size_t Lz, const T *members, std::size_t K, std::size_t L,
+                                     std::size_t D, double gamma, std::size_t bandwidth, const double *weights,
+                                     T *grad)
+    {
+        double value = 0;
+        if constexpr (sizeof(T) == 4)
+            check(sdtw_barycenter_objective_f32(ctx_, z, Lz, members, K, L, D, gamma, bandwidth, weights,
+                                                SDTW_PTR_HOST, &value, grad));
+        else
+            check(sdtw_barycenter_objective_f64(ctx_, z, Lz, members, K, L, D, gamma, bandwidth, weights,
+                                                SDTW_PTR_HOST, &value, grad));
+        return value;
+    }
+
+    // One Adam step (barycenter.hpp:181-191): fp64 moments, z updated in place.
+    template <class T>
+    void adam_step(T *z, const T *grad, double *m1, double *m2, std::size_t n, std::size_t t, double lr,
+                   double beta1, double beta2, double eps)
+    {
+        if constexpr (sizeof(T) == 4)
+            check(sdtw_adam_step_f32(ctx_, z, grad, m1, m2, n, t, lr, beta1, beta2, eps, SDTW_PTR_HOST));
+        else
+            check(sdtw_adam_step_f64(ctx_, z, grad, m1, m2, n, t, lr, beta1, beta2, eps, SDTW_PTR_HOST));
+    }
+
   private:
     template <class T>
     Output<T> run(const std::vector<T> &x, const std::vector<T> &y, std::size_t B, std::size_t N, std::size_t M,

@@ -1,8 +1,11 @@
 """The reference's C++ API on the engine (include/softdtw_b200/dropin.hpp):
-tests/cpp/conformance.cpp compares softdtw::b200::{sdtw_with_gradients,
-barycenter_objective} (fp32, GPU) with the unmodified reference's functions
-(T = double, CPU) and checks the reference's exception types and ledger
-semantics survive the drop-in."""
+tests/cpp/conformance.cpp compares softdtw::b200::{forward,
+forward_normalized, backward_log, backward_linear (both cost accessors),
+input_gradients, sdtw_with_gradients (log and linear space),
+barycenter_objective (ragged members), solve_barycenter} on the GPU with the
+unmodified reference's functions (T = double, CPU), and checks the
+reference's exception types (ValidationError, OutOfMemoryError,
+IncompleteTableError) and ledger semantics survive the drop-in."""
 import os
 import subprocess
 
