@@ -664,10 +664,10 @@ struct Pipeline {
         if (gx || gy) {
             // ordered, atomic-free contraction of the stored tiles
             Phase ph(ctx, 4);
-            const int ns = B * S, nc = B * C;
+            const int ns = B * S, nc = B * C, nkb = (D + 127) / 128;
             const unsigned cg = (unsigned)ctx->sm_count * 8;
             if (gx)
-                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(ns, cg), 256, 0, tiles.p,
+                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(ns * nkb, cg), 256, 0, tiles.p,
                        tile_meta.p, strip_tiles.p, tile_quota, nullptr, nullptr, 0, B, S, C, N, M, D, x, y, gx);
             if (gy) {
                 Buf<int> cnt(ctx, (size_t)nc), off(ctx, (size_t)nc + 1), ord(ctx, cap);
@@ -678,7 +678,7 @@ struct Pipeline {
                 LAUNCH(ctx, sdtw::tile_scatter_kernel, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C,
                        off.p, cnt.p, ord.p);
                 LAUNCH(ctx, sdtw::segment_sort_kernel, grid_for(nc, 128), 128, 0, off.p, ord.p, tile_meta.p, nc);
-                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(nc, cg), 256, 0, tiles.p,
+                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(nc * nkb, cg), 256, 0, tiles.p,
                        tile_meta.p, strip_tiles.p, tile_quota, off.p, ord.p, 1, B, S, C, N, M, D, y, x, gy);
             }
             if (need_fx) {

@@ -110,8 +110,14 @@ __global__ void segment_sort_kernel(const int *__restrict__ off, int *ord, const
 // 32 x 128 feature block: per partner index one 16-byte shared load of E and
 // one of p feed 16 FMAs.  Dot products accumulate in fp32 (fixed order), the
 // marginals and the final 2 (v marg - acc) in fp64.
+#ifndef CONTRACT_VOWN_EARLY
+#define CONTRACT_VOWN_EARLY 0
+#endif
+#ifndef CONTRACT_MIN_BLOCKS
+#define CONTRACT_MIN_BLOCKS 3
+#endif
 template <class T>
-__global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restrict__ tiles, const int4 *__restrict__ meta,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1) contract_ordered_kernel(const T *__restrict__ tiles, const int4 *__restrict__ meta,
                                                                const int *__restrict__ strip_tiles, int quota,
                                                                const int *__restrict__ off, const int *__restrict__ ord,
                                                                int which, int B, int S, int C, int N, int M, int D,
@@ -125,7 +131,11 @@ __global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restri
     const int og = tid >> 5, kg = tid & 31;  // rows 4 og .. +3, features 4 kg .. +3
     const int per_b = which == 0 ? S : C;
     const int Rout = which == 0 ? N : M, Rpart = which == 0 ? M : N;
-    for (int key = blockIdx.x; key < B * per_b; key += gridDim.x) {
+    // work item = (bucket, 128-feature block): at D = 1024 a bucket's eight
+    // feature blocks run on eight CTAs instead of one after the other
+    const int nkb = (D + 127) / 128;
+    for (int item = blockIdx.x; item < B * per_b * nkb; item += gridDim.x) {
+        const int key = item / nkb, kb = 128 * (item % nkb);
         const int b = key / per_b, blk = key % per_b;
         const int o0 = 32 * blk;
         const int lo = which == 0 ? key * quota : off[key];
@@ -133,13 +143,38 @@ __global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restri
         const T *vo = vout + (size_t)b * Rout * D;
         const T *vp = vpart + (size_t)b * Rpart * D;
         T *g = grad + (size_t)b * Rout * D;
-        for (int kb = 0; kb < D; kb += 128) {
+        if (lo == hi) {
+            // no non-zero E tile touches this block: the gradient is exactly 0
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int o = 4 * og + a;
+                if (o0 + o >= Rout) continue;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = kb + 4 * kg + q;
+                    if (k < D) g[(size_t)(o0 + o) * D + k] = T(0);
+                }
+            }
+            continue;
+        }
+#if CONTRACT_VOWN_EARLY
+        // the epilogue's own rows, loaded now so they arrive during the tiles
+        T vown[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int o = 4 * og + a, k = kb + 4 * kg + q;
+                vown[a][q] = (o0 + o < Rout && k < D) ? vo[(size_t)(o0 + o) * D + k] : T(0);
+            }
+#endif
+        {
             T acc[4][4];
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc[a][q] = T(0);
-            double marg[4] = {0.0, 0.0, 0.0, 0.0};
+            double marg_acc = 0.0;  // warp 0: marginal of output row tid
             // tile operands go through registers one tile ahead: the loads of
             // tile e + 1 are in flight while tile e is contracted
             T re[4], rp[16];
@@ -178,6 +213,13 @@ __global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restri
                 }
                 __syncthreads();
                 if (e + 1 < hi) load_tile(e + 1);
+                // marginals in fp64 (tile order, then partner order): warp 0,
+                // outside the FMA loop (no divergent fp64 adds in it)
+                if (tid < 32) {
+                    double mgt = marg_acc;
+                    for (int mm = 0; mm < np; ++mm) mgt += (double)Et[mm][tid];
+                    marg_acc = mgt;
+                }
                 for (int mm = 0; mm < np; ++mm) {
                     T ev[4], pv[4];
                     if constexpr (sizeof(T) == 4) {
@@ -192,20 +234,13 @@ __global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restri
                             pv[a] = P[mm][4 * kg + a];
                         }
                     }
-                    if (kb == 0 && kg == 0) {
-#pragma unroll
-                        for (int a = 0; a < 4; ++a) marg[a] += (double)ev[a];
-                    }
 #pragma unroll
                     for (int a = 0; a < 4; ++a)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) acc[a][q] = fma(ev[a], pv[q], acc[a][q]);
                 }
             }
-            if (kb == 0 && kg == 0) {
-#pragma unroll
-                for (int a = 0; a < 4; ++a) marg_s[4 * og + a] = marg[a];
-            }
+            if (tid < 32) marg_s[tid] = marg_acc;
             __syncthreads();
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
@@ -217,7 +252,11 @@ __global__ void __launch_bounds__(256) contract_ordered_kernel(const T *__restri
                     const int k = kb + 4 * kg + q;
                     if (k < D) {
                         const size_t id = (size_t)(o0 + o) * D + k;
+#if CONTRACT_VOWN_EARLY
+                        g[id] = (T)(2.0 * ((double)vown[a][q] * mg - (double)acc[a][q]));
+#else
                         g[id] = (T)(2.0 * ((double)vo[id] * mg - (double)acc[a][q]));
+#endif
                     }
                 }
             }
