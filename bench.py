@@ -531,18 +531,25 @@ def run_engine_arm(args, cfg):
                                   f"(sm_max_mhz, {src})",
                     "share_of_step": per_step[dom] / (total_ms / args.steps)}
     elif dom == "grads":
+        # the ordered contraction runs on the fp32 SIMT pipe (FFMA, fixed
+        # order for determinism), so its bound is the FFMA peak, computed
+        # like the MUFU one; algorithmic work counts only the stored non-zero
+        # tiles' cells would be smaller, so the dense 4 D flop/cell is quoted
         flop = 2 * 2 * cells_per_rank * D
         ach = flop / (per_step[dom] / 1e3) / 1e12
-        pk = float(peaks.get("bf16_tflops", 1590.0))
-        roofline = {"bound": "tensor", "kernel": "contract_ordered_kernel", "achieved": ach,
-                    "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
+        pk = SM_COUNT * 128 * 2 * sm_mhz * 1e6 / 1e12
+        roofline = {"bound": "fp32-fma", "kernel": "contract_ordered_kernel", "achieved": ach,
+                    "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": _traffic(args, dom),
+                    "algorithmic": f"4 D flop/cell (dX and dY, 2 flop per FMA) x {cells_per_rank} cells "
+                                   "(dense-equivalent: only non-zero E tiles are contracted)",
+                    "peak_basis": f"{SM_COUNT} SM x 128 FFMA/clk x 2 flop x {sm_mhz} MHz (sm_max_mhz, {src})",
                     "share_of_step": per_step[dom] / (total_ms / args.steps)}
     elif dom == "costs":
         byt = 4 * cells_per_rank
         ach = byt / (per_step[dom] / 1e3) / 1e9
         pk = float(peaks.get("hbm_gbs", 6650.0))
         roofline = {"bound": "hbm", "kernel": "cost_gemm_tc_kernel", "achieved": ach, "peak": pk,
-                    "unit": "GB/s", "frac": ach / pk, "traffic": None,
+                    "unit": "GB/s", "frac": ach / pk, "traffic": _traffic(args, dom),
                     "share_of_step": per_step[dom] / (total_ms / args.steps)}
 
     line = None
