@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
         // selects in every step instead of the fix-up path for the whole strip
         const bool r1 = s0 == 0 && t == 0;
         const bool has_rowN = 32 * (s0 + qlast + 1) >= a.N;
+        const bool strip_full = 32 * (s0 + qlast + 1) <= a.N;  // every lane's row exists
         unsigned long long pf_w = 0;  // prefetched halo entry (lanes 0..7)
         int pf_kb = -1;
         if (!kFused) {
@@ -302,7 +303,32 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                     if (t < n) halo_s[(kb + t) & 31] = hv;
                     __syncwarp();
                 }
-                if (fixup || tail) {
+                // Lean sub-group (one strip per warp, unfused): every lane's
+                // cell is interior and active (col in [1, M), full strip),
+                // not strip 0 (no row-1 selects) and no lane meets its
+                // diagonal cell here (no loss capture), so the step is the
+                // cell, the chunk-boundary capture and lane 31's store at an
+                // immediate offset: ~12 fewer instructions per step than the
+                // plain body below (same arithmetic, same results).
+                const bool lean = K == 1 && !kFused && !fixup && !tail && s0 > 0 && strip_full &&
+                                  kb >= 31 && kb + 7 < a.M && (kb + 7 < 32 * s0 || kb > 32 * s0 + 62);
+                if (lean) {
+                    const T *rgk = ring + (G & 1) * 1024 + k8 * 32 + t;
+                    typename TG::Ent *hp = A.hbt + ((size_t)b * a.S + s0) * a.M + (kb - 31);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int kl = k8 + kk;
+                        const T src = (t == 31) ? halo_s[kl] : h_prev[0];
+                        const T u = __shfl_sync(kFull, src, (t + 31) & 31);
+                        const T d = rgk[kk * 32];
+                        T g, v, h;
+                        fwd_cell<T>(d, u, l_carry[0], a.k, a.gln2, g, v, h);
+                        vck[0] = (kl == ((t - 1) & 31)) ? v : vck[0];
+                        l_carry[0] = v;
+                        h_prev[0] = h;
+                        TG::store_if(hp + kk, h, epoch, t == 31);
+                    }
+                } else if (fixup || tail) {
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
                         const int k = kb + kk;
