@@ -275,6 +275,7 @@ if (trc) {
     const int steps = a.M + 31;
     const bool r1 = row == 1;  // lane 0 of a pair's first strip: R(0, j) = inf
     const bool has_rowN = 32 * (s + 1) >= a.N;
+    const bool strip_full = 32 * (s + 1) <= a.N;  // every lane's row exists
     unsigned long long pf_w = 0;
     int pf_kb = -1;
     for (int k0 = 0; k0 < steps; k0 += 32) {
@@ -401,8 +402,41 @@ for (int k8 = 0; k8 < 32; k8 += 8) {
                              pub_local && t == 31 && active);
         }
     };
-    if (fixup || tail) steps8(std::true_type{});
-    else steps8(std::false_type{});
+    // lean sub-group: interior, every lane active (full strip, columns in
+    // [1, M)), not strip 0, no lane at its diagonal cell: the cell, the
+    // chunk-boundary capture and lane 31's two hand-off stores only (same
+    // arithmetic as the plain body, ~10 fewer instructions per step)
+    const bool lean = !fixup && !tail && s > 0 && strip_full && kb >= 31 && kb + 7 < a.M &&
+                      (kb + 7 < 32 * s || kb > 32 * s + 62);
+    if (lean) {
+        float hsv[8], dvv[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            hsv[kk] = halo_s[k8 + kk];
+            dvv[kk] = rg[(k8 + kk) * 32 + t];
+        }
+        typename TG::Ent *hp = hb_me + (kb - 31);
+        const unsigned pos0 = base + (unsigned)(kb - 31);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int kl = k8 + kk;
+            const float src = (t == 31) ? hsv[kk] : h_prev;
+            const float uu = __shfl_sync(kFull, src, (t + 31) & 31);
+            float g, v, h;
+            fwd_cell<float>(dvv[kk], uu, l_carry, a.k, a.gln2, g, v, h);
+            vck = (kl == ((t - 1) & 31)) ? v : vck;
+            l_carry = v;
+            h_prev = h;
+            TG::store_if(hp + kk, h, epoch, t == 31);
+            const unsigned pos = pos0 + (unsigned)kk;
+            st_shared_u64_if(hx_me + (pos & (kFtcHx - 1)), ((unsigned long long)pos << 32) | __float_as_uint(h),
+                             pub_local && t == 31);
+        }
+    } else if (fixup || tail) {
+        steps8(std::true_type{});
+    } else {
+        steps8(std::false_type{});
+    }
 }
 const int bidx = (t == 0) ? G : (G - 1);
 const int jb = 32 * (bidx + 1);
