@@ -292,6 +292,28 @@ int main()
             ze = std::max(ze, std::fabs(got.final_z.raw()[i] - ref.final_z.raw()[i]));
         CHECK(te <= 1e-9 && ze <= 1e-9, "solve_barycenter objective err %.3g, final z err %.3g", te, ze);
     }
+    // 11. run_bench_row (bench.hpp:52-107): same generator and row semantics
+    {
+        BenchConfigRow row;
+        row.batch = 2;
+        row.length = 64;
+        row.feature_dim = 8;
+        row.repeats = 2;
+        for (CostMode mode : {CostMode::unfused, CostMode::fused}) {
+            row.cost_mode = mode;
+            const auto ref = run_bench_row(row, 1);
+            const auto got = b200::run_bench_row(row);
+            CHECK(got.ok && ref.ok && got.peak_ledger_bytes > 0 && got.mean_runtime_ms > 0,
+                  "run_bench_row ok (%s)", got.error.c_str());
+            CHECK(std::fabs(got.loss0 - ref.loss0) <= 1e-5f * std::max(1.0f, std::fabs(ref.loss0)),
+                  "run_bench_row loss0 %.7g vs reference %.7g", got.loss0, ref.loss0);
+            CHECK(bench_csv_row(got).find(",ok") != std::string::npos, "bench CSV row status");
+        }
+        BenchConfigRow bad = row;
+        bad.length = 300;
+        const auto oom = b200::run_bench_row(bad, 0, 42, 4096);
+        CHECK(!oom.ok && !oom.error.empty(), "ledger limit recorded in the row, not thrown");
+    }
     std::printf("%s %d/%d checks\n", fails ? "FAIL" : "PASS", checks - fails, checks);
     return fails ? 1 : 0;
 }
