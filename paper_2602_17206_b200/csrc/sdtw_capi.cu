@@ -591,6 +591,11 @@ struct Pipeline {
             if (k >= 4) launch_forward3<4>();
             else if (k == 2) launch_forward3<2>();
             else launch_forward3<1>();
+        } else if (!fused) {
+            // one strip per warp: the lean step body (K == 1) beats strip ILP
+            // at every config measured (C5, 16384 strips: K=1 5.78 ms per Adam
+            // step, K=2 5.99, K=4 6.65)
+            launch_forward3<1>();
         } else if (strips >= 4 * slots) launch_forward3<4>();
         else if (strips >= 2 * slots) launch_forward3<2>();
         else launch_forward3<1>();
@@ -664,10 +669,13 @@ struct Pipeline {
         if (gx || gy) {
             // ordered, atomic-free contraction of the stored tiles
             Phase ph(ctx, 4);
-            const int ns = B * S, nc = B * C, nkb = (D + 127) / 128;
+            // feature blocks of 64 when D <= 64 (no zero-padded half), else 128
+            const int kw = D <= 64 ? 64 : 128;
+            const int ns = B * S, nc = B * C, nkb = (D + kw - 1) / kw;
             const unsigned cg = (unsigned)ctx->sm_count * 8;
+            auto contract = kw == 64 ? sdtw::contract_ordered_kernel<T, 64> : sdtw::contract_ordered_kernel<T, 128>;
             if (gx)
-                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(ns * nkb, cg), 256, 0, tiles.p,
+                LAUNCH(ctx, contract, std::min<unsigned>(ns * nkb, cg), 256, 0, tiles.p,
                        tile_meta.p, strip_tiles.p, tile_quota, nullptr, nullptr, 0, B, S, C, N, M, D, x, y, gx);
             if (gy) {
                 Buf<int> cnt(ctx, (size_t)nc), off(ctx, (size_t)nc + 1), ord(ctx, cap);
@@ -678,7 +686,7 @@ struct Pipeline {
                 LAUNCH(ctx, sdtw::tile_scatter_kernel, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C,
                        off.p, cnt.p, ord.p);
                 LAUNCH(ctx, sdtw::segment_sort_kernel, grid_for(nc, 128), 128, 0, off.p, ord.p, tile_meta.p, nc);
-                LAUNCH(ctx, sdtw::contract_ordered_kernel<T>, std::min<unsigned>(nc * nkb, cg), 256, 0, tiles.p,
+                LAUNCH(ctx, contract, std::min<unsigned>(nc * nkb, cg), 256, 0, tiles.p,
                        tile_meta.p, strip_tiles.p, tile_quota, off.p, ord.p, 1, B, S, C, N, M, D, y, x, gy);
             }
             if (need_fx) {

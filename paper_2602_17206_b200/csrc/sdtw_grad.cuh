@@ -110,32 +110,35 @@ __global__ void segment_sort_kernel(const int *__restrict__ off, int *ord, const
 // 32 x 128 feature block: per partner index one 16-byte shared load of E and
 // one of p feed 16 FMAs.  Dot products accumulate in fp32 (fixed order), the
 // marginals and the final 2 (v marg - acc) in fp64.
-#ifndef CONTRACT_VOWN_EARLY
-#define CONTRACT_VOWN_EARLY 0
-#endif
 #ifndef CONTRACT_MIN_BLOCKS
 #define CONTRACT_MIN_BLOCKS 3
 #endif
-template <class T>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1) contract_ordered_kernel(const T *__restrict__ tiles, const int4 *__restrict__ meta,
-                                                               const int *__restrict__ strip_tiles, int quota,
-                                                               const int *__restrict__ off, const int *__restrict__ ord,
-                                                               int which, int B, int S, int C, int N, int M, int D,
-                                                               const T *__restrict__ vout, const T *__restrict__ vpart,
-                                                               T *__restrict__ grad)
+// KW = feature-block width: 128, or 64 when D <= 64 (C5: D = 64), so that no
+// thread multiplies zero padding; each thread holds a RA (o) x 4 (k) block,
+// RA = KW / 32.  The per-element fp32 accumulation order (tiles in order,
+// partners in order) is the same for both widths.
+template <class T, int KW>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1)
+    contract_ordered_kernel(const T *__restrict__ tiles, const int4 *__restrict__ meta,
+                            const int *__restrict__ strip_tiles, int quota, const int *__restrict__ off,
+                            const int *__restrict__ ord, int which, int B, int S, int C, int N, int M, int D,
+                            const T *__restrict__ vout, const T *__restrict__ vpart, T *__restrict__ grad)
 {
+    constexpr int RA = KW / 32;          // output rows per thread
+    constexpr int KG = KW / 4;           // feature groups of 4
+    constexpr int NP = 32 * KW / 256;    // partner values staged per thread per tile
     __shared__ __align__(16) T Et[32][36];   // [m][o]
     __shared__ __align__(16) T P[32][132];   // [m][k]
     __shared__ double marg_s[32];
     const int tid = threadIdx.x;
-    const int og = tid >> 5, kg = tid & 31;  // rows 4 og .. +3, features 4 kg .. +3
+    const int og = tid / KG, kg = tid % KG;  // rows RA og .. +RA-1, features 4 kg .. +3
     const int per_b = which == 0 ? S : C;
     const int Rout = which == 0 ? N : M, Rpart = which == 0 ? M : N;
-    // work item = (bucket, 128-feature block): at D = 1024 a bucket's eight
+    // work item = (bucket, KW-feature block): at D = 1024 a bucket's eight
     // feature blocks run on eight CTAs instead of one after the other
-    const int nkb = (D + 127) / 128;
+    const int nkb = (D + KW - 1) / KW;
     for (int item = blockIdx.x; item < B * per_b * nkb; item += gridDim.x) {
-        const int key = item / nkb, kb = 128 * (item % nkb);
+        const int key = item / nkb, kb = KW * (item % nkb);
         const int b = key / per_b, blk = key % per_b;
         const int o0 = 32 * blk;
         const int lo = which == 0 ? key * quota : off[key];
@@ -146,8 +149,8 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1)
         if (lo == hi) {
             // no non-zero E tile touches this block: the gradient is exactly 0
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int o = 4 * og + a;
+            for (int a = 0; a < RA; ++a) {
+                const int o = RA * og + a;
                 if (o0 + o >= Rout) continue;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -157,107 +160,95 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1)
             }
             continue;
         }
-#if CONTRACT_VOWN_EARLY
-        // the epilogue's own rows, loaded now so they arrive during the tiles
-        T vown[4][4];
+        T acc[RA][4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < RA; ++a)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int o = 4 * og + a, k = kb + 4 * kg + q;
-                vown[a][q] = (o0 + o < Rout && k < D) ? vo[(size_t)(o0 + o) * D + k] : T(0);
+            for (int q = 0; q < 4; ++q) acc[a][q] = T(0);
+        double marg_acc = 0.0;  // warp 0: marginal of output row tid
+        // tile operands go through registers one tile ahead: the loads of
+        // tile e + 1 are in flight while tile e is contracted
+        T re[4], rp[NP];
+        int np_next = 0;
+        auto load_tile = [&](int e) {
+            const int idx = which == 0 ? e : ord[e];
+            const int4 m = meta[idx];
+            const T *et = tiles + (size_t)idx * 1024;  // [r][jj]
+            const int p0 = which == 0 ? 32 * m.z : 32 * m.y;
+            const int np = which == 0 ? m.w : min(32, N - 32 * m.y);
+            np_next = np;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) re[q] = et[tid + 256 * q];
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const int u = tid + 256 * q;
+                const int r = u / KW, k = u % KW;
+                rp[q] = (r < np && kb + k < D) ? vp[(size_t)(p0 + r) * D + kb + k] : T(0);
             }
-#endif
-        {
-            T acc[4][4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[a][q] = T(0);
-            double marg_acc = 0.0;  // warp 0: marginal of output row tid
-            // tile operands go through registers one tile ahead: the loads of
-            // tile e + 1 are in flight while tile e is contracted
-            T re[4], rp[16];
-            int np_next = 0;
-            auto load_tile = [&](int e) {
-                const int idx = which == 0 ? e : ord[e];
-                const int4 m = meta[idx];
-                const T *et = tiles + (size_t)idx * 1024;  // [r][jj]
-                const int p0 = which == 0 ? 32 * m.z : 32 * m.y;
-                const int np = which == 0 ? m.w : min(32, N - 32 * m.y);
-                np_next = np;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) re[q] = et[tid + 256 * q];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int u = tid + 256 * q;
-                    const int r = u >> 7, k = u & 127;
-                    rp[q] = (r < np && kb + k < D) ? vp[(size_t)(p0 + r) * D + kb + k] : T(0);
-                }
-            };
-            if (lo < hi) load_tile(lo);
-            for (int e = lo; e < hi; ++e) {
-                const int np = np_next;
-                __syncthreads();
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int u = tid + 256 * q;
-                    const int r = u >> 5, jj = u & 31;
-                    if (which == 0) Et[jj][r] = re[q];  // o = r, m = jj
-                    else Et[r][jj] = re[q];             // o = jj, m = r
-                }
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int u = tid + 256 * q;
-                    P[u >> 7][u & 127] = rp[q];
-                }
-                __syncthreads();
-                if (e + 1 < hi) load_tile(e + 1);
-                // marginals in fp64 (tile order, then partner order): warp 0,
-                // outside the FMA loop (no divergent fp64 adds in it)
-                if (tid < 32) {
-                    double mgt = marg_acc;
-                    for (int mm = 0; mm < np; ++mm) mgt += (double)Et[mm][tid];
-                    marg_acc = mgt;
-                }
-                for (int mm = 0; mm < np; ++mm) {
-                    T ev[4], pv[4];
-                    if constexpr (sizeof(T) == 4) {
-                        const float4 e4 = *reinterpret_cast<const float4 *>(&Et[mm][4 * og]);
-                        const float4 p4 = *reinterpret_cast<const float4 *>(&P[mm][4 * kg]);
-                        ev[0] = e4.x; ev[1] = e4.y; ev[2] = e4.z; ev[3] = e4.w;
-                        pv[0] = p4.x; pv[1] = p4.y; pv[2] = p4.z; pv[3] = p4.w;
-                    } else {
-#pragma unroll
-                        for (int a = 0; a < 4; ++a) {
-                            ev[a] = Et[mm][4 * og + a];
-                            pv[a] = P[mm][4 * kg + a];
-                        }
-                    }
-#pragma unroll
-                    for (int a = 0; a < 4; ++a)
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) acc[a][q] = fma(ev[a], pv[q], acc[a][q]);
-                }
-            }
-            if (tid < 32) marg_s[tid] = marg_acc;
+        };
+        load_tile(lo);
+        for (int e = lo; e < hi; ++e) {
+            const int np = np_next;
             __syncthreads();
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int o = 4 * og + a;
-                if (o0 + o >= Rout) continue;
-                const double mg = marg_s[o];
+            for (int q = 0; q < 4; ++q) {
+                const int u = tid + 256 * q;
+                const int r = u >> 5, jj = u & 31;
+                if (which == 0) Et[jj][r] = re[q];  // o = r, m = jj
+                else Et[r][jj] = re[q];             // o = jj, m = r
+            }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int k = kb + 4 * kg + q;
-                    if (k < D) {
-                        const size_t id = (size_t)(o0 + o) * D + k;
-#if CONTRACT_VOWN_EARLY
-                        g[id] = (T)(2.0 * ((double)vown[a][q] * mg - (double)acc[a][q]));
-#else
-                        g[id] = (T)(2.0 * ((double)vo[id] * mg - (double)acc[a][q]));
-#endif
-                    }
+            for (int q = 0; q < NP; ++q) {
+                const int u = tid + 256 * q;
+                P[u / KW][u % KW] = rp[q];
+            }
+            __syncthreads();
+            if (e + 1 < hi) load_tile(e + 1);
+            // marginals in fp64 (tile order, then partner order): warp 0,
+            // outside the FMA loop (no divergent fp64 adds in it)
+            if (tid < 32) {
+                double mgt = marg_acc;
+                for (int mm = 0; mm < np; ++mm) mgt += (double)Et[mm][tid];
+                marg_acc = mgt;
+            }
+            for (int mm = 0; mm < np; ++mm) {
+                T ev[RA], pv[4];
+                if constexpr (sizeof(T) == 4 && RA == 4) {
+                    const float4 e4 = *reinterpret_cast<const float4 *>(&Et[mm][4 * og]);
+                    ev[0] = e4.x; ev[1] = e4.y; ev[2] = e4.z; ev[3] = e4.w;
+                } else if constexpr (sizeof(T) == 4 && RA == 2) {
+                    const float2 e2 = *reinterpret_cast<const float2 *>(&Et[mm][2 * og]);
+                    ev[0] = e2.x; ev[1] = e2.y;
+                } else {
+#pragma unroll
+                    for (int a = 0; a < RA; ++a) ev[a] = Et[mm][RA * og + a];
+                }
+                if constexpr (sizeof(T) == 4) {
+                    const float4 p4 = *reinterpret_cast<const float4 *>(&P[mm][4 * kg]);
+                    pv[0] = p4.x; pv[1] = p4.y; pv[2] = p4.z; pv[3] = p4.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) pv[q] = P[mm][4 * kg + q];
+                }
+#pragma unroll
+                for (int a = 0; a < RA; ++a)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[a][q] = fma(ev[a], pv[q], acc[a][q]);
+            }
+        }
+        if (tid < 32) marg_s[tid] = marg_acc;
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            const int o = RA * og + a;
+            if (o0 + o >= Rout) continue;
+            const double mg = marg_s[o];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = kb + 4 * kg + q;
+                if (k < D) {
+                    const size_t id = (size_t)(o0 + o) * D + k;
+                    g[id] = (T)(2.0 * ((double)vo[id] * mg - (double)acc[a][q]));
                 }
             }
         }
