@@ -186,8 +186,10 @@ __device__ __forceinline__ Cell<T> dp_cell(int i, int j, int bw, T d, T u, T l,
     const T s = (e0 + eu) + el;
     const T sm = mn - gln2 * Num<T>::lg2(s);
     c.g = d + sm;
-    c.v = c.g - u;
-    c.h = c.g - l;
+    // the same rounding as fwd_cell / prob_cell: a tile recomputed through
+    // this general cell or through the branch-free one gives identical bits
+    c.v = (d - u) + sm;
+    c.h = (d - l) + sm;
     if (kProbs) {
         // One Newton step makes the three probabilities sum to 1 within an
         // ulp; an approximate reciprocal's bias would otherwise compound

@@ -39,6 +39,15 @@ enum : unsigned { kTileDead = 1u, kTileHint = 2u, kTileLive = 3u, kTileCommit = 
 #endif
 constexpr unsigned kSpecDepth = 2;
 
+// Recompute window: tiles per recompute request (ILP of the helper's skewed
+// loop); the probability cache holds two windows.  3 for the tensor-core
+// fused path (TMEM limits it to one CTA per SM anyway), 2 otherwise: the
+// 4-slot cache (51 KB) fits three workers per SM instead of two, so 1.5x
+// more strips are in flight (the backward is occupancy-bound at C3 / C5:
+// 4096 / 16384 strips against 296 workers).
+template <bool kTc>
+constexpr int bwd_window() { return kTc ? 3 : 2; }
+
 template <class T, bool kFused, bool kTc = false>
 struct Bwd4Smem {
     // kTc: the strip's x rows as a packed fp16 hi/lo tensor-core operand
@@ -46,7 +55,7 @@ struct Bwd4Smem {
     // the M = 128 MMA read (harmlessly) into the probability slots after it
     static constexpr int kX = kTc ? kFtcMaxD * 32 * 4 / (int)sizeof(T) : 0;
     static constexpr int kSlot = 3 * 33 * 32;            // pd, pu, pl [jj][t], row 32 = dummy
-    static constexpr int kP = 6 * kSlot;                 // two groups of three probability tiles
+    static constexpr int kP = 2 * bwd_window<kTc>() * kSlot;  // two windows of probability tiles
     static constexpr int kE = 32 * 34;                   // E tile [t][jj] (even stride: conflict-free), column 32 = dummy
     static constexpr int kRing = (kFused && !kTc) ? 0 : 4 * 1024;  // skewed cost row groups (slot g & 3)
     static constexpr int kHalo = 6 * 32;                 // 3 top halos (h), S in, S out (+dummy)
@@ -118,6 +127,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ uint32_t tmem_slot;
     constexpr int kW = bwd_workers<kTc>();
+    constexpr int kWin = bwd_window<kTc>();
     const DpArgs<T> &a = A.a;
     using SM = Bwd4Smem<T, kFused, kTc>;
     using TG = Tagged<T>;
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
         auto group_of = [&](int cf) {
             for (int g = 0; g < 2; ++g) {
                 const int w0 = ctl[5 + g];
-                if (ctl[7 + g] != 0 && cf <= w0 && cf > w0 - 3 && cf >= 0) return g;
+                if (ctl[7 + g] != 0 && cf <= w0 && cf > w0 - kWin && cf >= 0) return g;
             }
             return -1;
         };
@@ -238,7 +248,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
             if constexpr (kTc) {
                 const int dpad = F.dpad;
                 // operand staging inside the target group's own slots (free)
-                uint8_t *stage = reinterpret_cast<uint8_t *>(base + kSlot * 3 * grp);
+                uint8_t *stage = reinterpret_cast<uint8_t *>(base + kSlot * kWin * grp);
                 const uint32_t idesc = tc::idesc_f16_f32(128, 32);
                 const SplitScale sc = split_scale(A.absmax);
                 // raw fp32 staging after the three fp16 operand tiles (the
@@ -359,17 +369,17 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
             ev(1, cr);
             lap(5);
             const int wr = min(32, a.M - 32 * cr);
-            const int nt = min(3, cr + 1);
+            const int nt = min(kWin, cr + 1);
             if constexpr (kTc) {
                 tc_costs(cr, nt, x_loaded, b, s, i, row_ok, tc_xi);
             } else if (!kFused) {
-                for (int g = cr - 2; g <= cr + 1; ++g)
+                for (int g = cr - (kWin - 1); g <= cr + 1; ++g)
                     if (g >= 0 && g < ngroups_row) load_group(ring + (g & 3) * 1024, dsrc + (size_t)g * 1024, t);
                 cp_async_commit();
             }
-            T lc[3], hp[3];
+            T lc[kWin], hp[kWin];
 #pragma unroll
-            for (int z = 0; z < 3; ++z) {
+            for (int z = 0; z < kWin; ++z) {
                 const int cz = cr - z;
                 lc[z] = (z < nt && cz > 0 && row_ok) ? a.vc[((size_t)b * a.C + (cz - 1)) * a.N + (i - 1)] : T(0);
                 hp[z] = T(0);
@@ -386,12 +396,12 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
             // 8-step sub-groups (64 steps; the last is a no-op): costs and top
             // halos of the sub-group loaded up front, branch-free steps
             for (int q8 = 0; q8 < 64; q8 += 8) {
-                T d8[3][8], hs8[3][8];
+                T d8[kWin][8], hs8[kWin][8];
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const int q = q8 + kk;
 #pragma unroll
-                    for (int z = 0; z < 3; ++z) {
+                    for (int z = 0; z < kWin; ++z) {
                         hs8[z][kk] = halo_s[z * 32 + (q & 31)];
                         // skewed row 32 (cr - z) + q of the ring
                         d8[z][kk] = kFused ? T(0) : ring[((cr - z + (q >> 5)) & 3) * 1024 + (q & 31) * 32 + t];
@@ -402,14 +412,14 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
                         const int q = q8 + kk;
-                        T src[3], u[3];
+                        T src[kWin], u[kWin];
 #pragma unroll
-                        for (int z = 0; z < 3; ++z) src[z] = (t == 31) ? hs8[z][kk] : hp[z];
+                        for (int z = 0; z < kWin; ++z) src[z] = (t == 31) ? hs8[z][kk] : hp[z];
 #pragma unroll
-                        for (int z = 0; z < 3; ++z) u[z] = __shfl_sync(kFull, src[z], (t + 31) & 31);
+                        for (int z = 0; z < kWin; ++z) u[z] = __shfl_sync(kFull, src[z], (t + 31) & 31);
                         const int jj = q - t;
 #pragma unroll
-                        for (int z = 0; z < 3; ++z) {
+                        for (int z = 0; z < kWin; ++z) {
                             const int wz = z == 0 ? wr : 32;
                             const bool act = z < nt && row_ok && jj >= 0 && jj < wz;
                             const int j = 32 * (cr - z) + 1 + jj;
@@ -422,7 +432,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                                 prob_cell<T>(d, u[z], lc[z], a.k, a.gln2, v, h, pd, pu, pl);
                             }
                             // inactive lanes write the dummy row: no divergent branch
-                            T *Pz = base + kSlot * (3 * grp + z) + (act ? jj : 32) * 32 + t;
+                            T *Pz = base + kSlot * (kWin * grp + z) + (act ? jj : 32) * 32 + t;
                             Pz[0] = pd;
                             Pz[1056] = pu;
                             Pz[2112] = pl;
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
         auto pick_group = [&]() {
             const int e_pos = ctl[4];
             for (int g = 0; g < 2; ++g)
-                if (ctl[7 + g] == 0 || ctl[5 + g] - 2 > e_pos) return g;  // empty or passed by E
+                if (ctl[7 + g] == 0 || ctl[5 + g] - (kWin - 1) > e_pos) return g;  // empty or passed by E
             return ctl[5] < ctl[6] ? 0 : 1;                                 // else the leftmost (speculative)
         };
         auto serve = [&](int cr) {
@@ -472,12 +482,12 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                 for (int g = 0; g < 2; ++g)
                     if (ctl[7 + g] != 0) w = min(w, ctl[5 + g]);
                 const int e_pos = ctl[4];
-                if (w != (1 << 30) && w - 3 >= 0 && w - 3 <= e_pos) {
+                if (w != (1 << 30) && w - kWin >= 0 && w - kWin <= e_pos) {
                     // only into a group E no longer needs
                     bool free_g = false;
                     for (int g = 0; g < 2; ++g)
-                        free_g |= ctl[7 + g] == 0 || ctl[5 + g] - 2 > e_pos;
-                    if (free_g) cn = w - 3;
+                        free_g |= ctl[7 + g] == 0 || ctl[5 + g] - (kWin - 1) > e_pos;
+                    if (free_g) cn = w - kWin;
                 }
             }
             cn = __shfl_sync(kFull, cn, 0);
@@ -512,7 +522,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                 w0 = __shfl_sync(kFull, w0, 0);
                 if (g >= 0 && st == 2) {
                     __threadfence_block();
-                    return base + kSlot * (3 * g + (w0 - cf));
+                    return base + kSlot * (kWin * g + (w0 - cf));
                 }
                 if (g < 0 && !requested) {
                     request(cf);
