@@ -314,6 +314,26 @@ int main()
         const auto oom = b200::run_bench_row(bad, 0, 42, 4096);
         CHECK(!oom.ok && !oom.error.empty(), "ledger limit recorded in the row, not thrown");
     }
+    // 12. series files (io.hpp: SDTW v1 binary and CSV) feed the drop-in
+    //     unchanged: the reference's own readers produce the SeriesBatch the
+    //     engine consumes
+    {
+        auto x = randn<double>(1, 45, 3, 61), y = randn<double>(1, 52, 3, 62);
+        const std::string bx = "/tmp/sdtw_b200_conf_x.bin", cy = "/tmp/sdtw_b200_conf_y.csv";
+        write_series_binary(bx, x);
+        write_series_csv(cy, y);
+        auto xr = read_series<double>(bx), yr = read_series<double>(cy);
+        SdtwConfig cfg;
+        cfg.gamma = 0.5;
+        auto ref = sdtw_with_gradients(xr, yr, cfg);
+        auto got = b200::sdtw_with_gradients(xr, yr, cfg);
+        double e = std::fabs(got.loss[0] - ref.loss[0]);
+        for (std::size_t i = 0; i < ref.grads.grad_x.size(); ++i)
+            e = std::max(e, std::fabs(got.grads.grad_x[i] - ref.grads.grad_x[i]));
+        CHECK(xr.raw() == x.raw() && e <= 1e-9, "series files through the drop-in: err %.3g", e);
+        std::remove(bx.c_str());
+        std::remove(cy.c_str());
+    }
     std::printf("%s %d/%d checks\n", fails ? "FAIL" : "PASS", checks - fails, checks);
     return fails ? 1 : 0;
 }
