@@ -661,8 +661,16 @@ struct Pipeline {
                 const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);
                 LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, sdtw::FusedTcArgs{});
             } else {
-                auto kern = sdtw::sdtw_backward4_kernel<T, false>;
-                const size_t smem = sdtw::Bwd4Smem<T, false>::kPerWarp * sizeof(T);
+                // recompute window: 3 tiles per request where alignment bands
+                // are narrow and strips few (C2: 0.447 vs 0.455 ms, C3: 1.63
+                // vs 1.72 ms), 2 (three workers per SM) where bands are wide
+                // or strips many (C1 backward -16 %, C5 -25 %)
+                const bool win2 = gamma >= 0.5 || (size_t)B * S > 8192;
+                auto kern = win2 ? sdtw::sdtw_backward4_kernel<T, false, false, 2>
+                                 : sdtw::sdtw_backward4_kernel<T, false, false, 3>;
+                const size_t smem = (win2 ? sdtw::Bwd4Smem<T, false, false, 2>::kPerWarp
+                                          : sdtw::Bwd4Smem<T, false, false, 3>::kPerWarp) *
+                                    sizeof(T);
                 LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, sdtw::FusedTcArgs{});
             }
         }
@@ -677,7 +685,11 @@ struct Pipeline {
             if (gx)
                 LAUNCH(ctx, contract, std::min<unsigned>(ns * nkb, cg), 256, 0, tiles.p,
                        tile_meta.p, strip_tiles.p, tile_quota, nullptr, nullptr, 0, B, S, C, N, M, D, x, y, gx);
-            if (gy) {
+            if (gy && S <= sdtw::max_list_strips<T>()) {
+                // chunk buckets built inside the contraction (strip order)
+                LAUNCH(ctx, contract, std::min<unsigned>(nc * nkb, cg), 256, 0, tiles.p, tile_meta.p, strip_tiles.p,
+                       tile_quota, nullptr, nullptr, 1, B, S, C, N, M, D, y, x, gy);
+            } else if (gy) {
                 Buf<int> cnt(ctx, (size_t)nc), off(ctx, (size_t)nc + 1), ord(ctx, cap);
                 CUDA_OK(cudaMemsetAsync(cnt.p, 0, cnt.n * sizeof(int), ctx->stream));
                 const unsigned tg = grid_for(cap, 256, (unsigned)ctx->sm_count * 8);

@@ -48,14 +48,14 @@ constexpr unsigned kSpecDepth = 2;
 template <bool kTc>
 constexpr int bwd_window() { return kTc ? 3 : 2; }
 
-template <class T, bool kFused, bool kTc = false>
+template <class T, bool kFused, bool kTc = false, int kWin = bwd_window<kTc>()>
 struct Bwd4Smem {
     // kTc: the strip's x rows as a packed fp16 hi/lo tensor-core operand
     // (32 rows x kFtcMaxD), placed first so that the unused rows 32..127 of
     // the M = 128 MMA read (harmlessly) into the probability slots after it
     static constexpr int kX = kTc ? kFtcMaxD * 32 * 4 / (int)sizeof(T) : 0;
     static constexpr int kSlot = 3 * 33 * 32;            // pd, pu, pl [jj][t], row 32 = dummy
-    static constexpr int kP = 2 * bwd_window<kTc>() * kSlot;  // two windows of probability tiles
+    static constexpr int kP = 2 * kWin * kSlot;          // two windows of probability tiles
     static constexpr int kE = 32 * 34;                   // E tile [t][jj] (even stride: conflict-free), column 32 = dummy
     static constexpr int kRing = (kFused && !kTc) ? 0 : 4 * 1024;  // skewed cost row groups (slot g & 3)
     static constexpr int kHalo = 6 * 32;                 // 3 top halos (h), S in, S out (+dummy)
@@ -119,7 +119,7 @@ __device__ __forceinline__ T bwd_cost(const DpArgs<T> &a, const T *ring, int b, 
 template <bool kTc>
 constexpr int bwd_workers() { return kTc ? 2 : 1; }
 
-template <class T, bool kFused, bool kTc = false>
+template <class T, bool kFused, bool kTc = false, int kWin = bwd_window<kTc>()>
 __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_kernel(Dp3Args<T> A,
                                                                                    unsigned long long *stat,
                                                                                    FusedTcArgs F)
@@ -127,9 +127,8 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ uint32_t tmem_slot;
     constexpr int kW = bwd_workers<kTc>();
-    constexpr int kWin = bwd_window<kTc>();
     const DpArgs<T> &a = A.a;
-    using SM = Bwd4Smem<T, kFused, kTc>;
+    using SM = Bwd4Smem<T, kFused, kTc, kWin>;
     using TG = Tagged<T>;
     const int t = threadIdx.x & 31;
     const int wk = (threadIdx.x >> 5) % kW;    // worker

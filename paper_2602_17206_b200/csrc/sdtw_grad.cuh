@@ -110,6 +110,10 @@ __global__ void segment_sort_kernel(const int *__restrict__ off, int *ord, const
 // 32 x 128 feature block: per partner index one 16-byte shared load of E and
 // one of p feed 16 FMAs.  Dot products accumulate in fp32 (fixed order), the
 // marginals and the final 2 (v marg - acc) in fp64.
+// strips per pair the in-kernel chunk bucketing handles (static shared memory)
+template <class T>
+constexpr int max_list_strips() { return sizeof(T) == 4 ? 2048 : 256; }
+
 #ifndef CONTRACT_MIN_BLOCKS
 #define CONTRACT_MIN_BLOCKS 3
 #endif
@@ -130,6 +134,11 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1)
     __shared__ __align__(16) T Et[32][36];   // [m][o]
     __shared__ __align__(16) T P[32][132];   // [m][k]
     __shared__ double marg_s[32];
+    // which = 1 without a global bucket sort (ord == nullptr, S <= list size):
+    // the chunk's tiles in strip order, found by scanning the strips' own
+    // tile lists (each strip holds at most one tile of a chunk)
+    __shared__ int lst[max_list_strips<T>()];
+    __shared__ int wcnt[8];
     const int tid = threadIdx.x;
     const int og = tid / KG, kg = tid % KG;  // rows RA og .. +RA-1, features 4 kg .. +3
     const int per_b = which == 0 ? S : C;
@@ -141,8 +150,43 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1)
         const int key = item / nkb, kb = KW * (item % nkb);
         const int b = key / per_b, blk = key % per_b;
         const int o0 = 32 * blk;
-        const int lo = which == 0 ? key * quota : off[key];
-        const int hi = which == 0 ? lo + strip_tiles[key] : off[key + 1];
+        int lo, hi;
+        const int *ordp = ord;
+        if (which == 0) {
+            lo = key * quota;
+            hi = lo + strip_tiles[key];
+        } else if (ord) {
+            lo = off[key];
+            hi = off[key + 1];
+        } else {
+            // ordered compaction, 256 strips at a time
+            int n = 0;
+            for (int sb = 0; sb < S; sb += 256) {
+                const int s = sb + tid;
+                int found = -1;
+                if (s < S) {
+                    const int ks = b * S + s, nt = strip_tiles[ks];
+                    for (int q = 0; q < nt; ++q)
+                        if (meta[ks * quota + q].z == blk) {
+                            found = ks * quota + q;
+                            break;
+                        }
+                }
+                const unsigned bal = __ballot_sync(kFull, found >= 0);
+                const int w = tid >> 5, ln = tid & 31;
+                __syncthreads();  // lst / wcnt of the previous round consumed
+                if (ln == 0) wcnt[w] = __popc(bal);
+                __syncthreads();
+                int pre = n;
+                for (int q = 0; q < w; ++q) pre += wcnt[q];
+                if (found >= 0) lst[pre + __popc(bal & ((1u << ln) - 1u))] = found;
+                for (int q = 0; q < 8; ++q) n += wcnt[q];
+            }
+            __syncthreads();
+            lo = 0;
+            hi = n;
+            ordp = lst;
+        }
         const T *vo = vout + (size_t)b * Rout * D;
         const T *vp = vpart + (size_t)b * Rpart * D;
         T *g = grad + (size_t)b * Rout * D;
@@ -171,7 +215,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? CONTRACT_MIN_BLOCKS : 1)
         T re[4], rp[NP];
         int np_next = 0;
         auto load_tile = [&](int e) {
-            const int idx = which == 0 ? e : ord[e];
+            const int idx = which == 0 ? e : ordp[e];
             const int4 m = meta[idx];
             const T *et = tiles + (size_t)idx * 1024;  // [r][jj]
             const int p0 = which == 0 ? 32 * m.z : 32 * m.y;
