@@ -332,7 +332,11 @@ constexpr int kCgPitch = 162;
 constexpr int kCgStageBytes = 32768 + 40960;                  // one round's operands: A 32 KB + B 40 KB
 constexpr int kCgEpiBytes = 4 * 32 * kCgPitch * 4;            // epilogue staging (81 KB)
 constexpr int kCgSmem = 2 * kCgStageBytes + kCgEpiBytes;      // 225 KB: two operand stages + staging
-constexpr int kCgThreads = 288;                               // 8 epilogue warps + 1 producer warp
+#ifndef CG_EPI_WARPS
+#define CG_EPI_WARPS 12  // measured: 8 -> 0.808, 12 -> 0.772, 16 -> 0.804 ms at C3
+#endif
+constexpr int kCgEpiWarps = CG_EPI_WARPS;                     // epilogue warps (3 per TMEM lane quarter)
+constexpr int kCgThreads = 32 * (kCgEpiWarps + 1);            // + 1 producer warp
 
 struct CgShared {
     uint64_t st_full[2], st_empty[2], acc_full[2], acc_empty[2];
@@ -341,7 +345,7 @@ struct CgShared {
 
 // Persistent and pipelined: TMEM kernels run one CTA per SM, so each CTA
 // walks tiles (b, ib, jb) with the producer warp loading round g + 1 while
-// the MMAs of round g run, and the eight epilogue warps draining tile n - 1
+// the MMAs of round g run, and the epilogue warps draining tile n - 1
 // from the other TMEM accumulator (2 x 160 columns) while tile n is computed.
 __global__ void __launch_bounds__(kCgThreads, 1)
     cost_gemm_tc_kernel(const uint8_t *__restrict__ xp, const uint8_t *__restrict__ yp, const float *__restrict__ xn,
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             tc::mbar_init(&sh.st_full[k], 1);
             tc::mbar_init(&sh.st_empty[k], 1);
             tc::mbar_init(&sh.acc_full[k], 1);
-            tc::mbar_init(&sh.acc_empty[k], 8);
+            tc::mbar_init(&sh.acc_empty[k], kCgEpiWarps);
         }
         tc::fence_barrier_init();
     }
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(kCgThreads, 1)
         b = r / NB;
     };
 
-    if (warp == 8) {
+    if (warp == kCgEpiWarps) {
         // ---------------------------------------------------------------- producer
         if (lane == 0) {
             const uint32_t idesc = tc::idesc_f16_f32(128, 160);
@@ -432,11 +436,12 @@ __global__ void __launch_bounds__(kCgThreads, 1)
     } else {
         // ---------------------------------------------------------------- epilogue
         // warp w reads TMEM lane quarter q = w & 3 (rows i0 + 32 q + lane);
-        // warps 0-3 take chunks z = 0..2, warps 4-7 chunks 3..4
+        // the G warps of a quarter split its five 32-column chunks
+        constexpr int G = kCgEpiWarps / 4;  // warps per lane quarter
         const int q = warp & 3, hf = warp >> 2;
         float *stage = reinterpret_cast<float *>(smem + 2 * kCgStageBytes) + q * 32 * kCgPitch;
         const float m2 = -2.0f * sc.inv;
-        const int zb = hf == 0 ? 0 : 3, ze = hf == 0 ? 3 : 5;
+        const int zb = (5 * hf) / G, ze = (5 * (hf + 1)) / G;  // this warp's 32-column chunks
         int li = 0;
         for (int n = blockIdx.x; n < ntiles; n += gridDim.x, ++li) {
             int b, ib, jb;
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             tc::mbar_wait(&sh.acc_full[ab], (li >> 1) & 1);
             tc::tc_fence_after();
             // the staging area is free once every epilogue warp finished the previous tile
-            named_bar_cg(1, 256);
+            named_bar_cg(1, 32 * kCgEpiWarps);
             const bool interior = j0 >= 32 && j0 + 128 <= M && bw == 0 && i0 + 128 <= N;
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
@@ -482,15 +487,15 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sh.acc_empty[ab]);
-            named_bar_cg(1, 256);
+            named_bar_cg(1, 32 * kCgEpiWarps);
             const int s = 4 * ib + q;
             if (32 * s < N) {
                 float *ds = dsk + ((size_t)b * S + s) * (size_t)KK * 32;
                 const bool last = jb == JB - 1;
                 const int rend = last ? KK : min(j0 + 128, KK);
                 const int t4 = 4 * (lane & 7);
-                // the two warps of a lane quarter take alternate groups of 4 rows
-                for (int kk0 = j0 + 4 * hf; kk0 < rend; kk0 += 8) {
+                // the G warps of a lane quarter take interleaved groups of 4 rows
+                for (int kk0 = j0 + 4 * hf; kk0 < rend; kk0 += 4 * G) {
                     const int kk = kk0 + (lane >> 3);
                     const float *sr = stage + kk - j0 + 32;
                     float v[4];
