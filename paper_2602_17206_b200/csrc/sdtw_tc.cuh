@@ -127,6 +127,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// 1-D bulk copy shared -> global (TMA engine), tracked by the thread's bulk group.
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the thread's bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// the thread's bulk stores are complete
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // 32 lanes x 32 consecutive fp32 columns: thread t gets lane (base+t), columns
 // [col, col+32).  The warp must own the lane quarter (warp_id % 4).
@@ -323,14 +335,14 @@ __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, i
 // write whole rows of the DP's skewed strip layout
 //   dsk[b][s][kk][t] = d(32 s + t, kk - t)   (0-based, kk in [0, KK))
 // for kk in [j0, j0 + 128) with no row shared between CTAs: the epilogue
-// stages each warp's 32 x 160 block in shared memory (pitch 162: the skewed
-// reads are bank-conflict free) and writes four skewed rows (512 contiguous
-// bytes) per 16-byte store.  The last column block also writes the tail rows
-// up to KK.
+// writes each strip's costs into a shared-memory image of those skewed rows
+// (bank-conflict free) and sends the image, contiguous in dsk, to HBM with one
+// bulk store (TMA engine) that overlaps the next tile's epilogue.  The last
+// column block also writes the tail rows up to KK.
 // ----------------------------------------------------------------------------
-constexpr int kCgPitch = 162;
+constexpr int kCgStageRows = 160;                             // skewed rows per strip image (KK - j0 <= 160)
 constexpr int kCgStageBytes = 32768 + 40960;                  // one round's operands: A 32 KB + B 40 KB
-constexpr int kCgEpiBytes = 4 * 32 * kCgPitch * 4;            // epilogue staging (81 KB)
+constexpr int kCgEpiBytes = 4 * kCgStageRows * 32 * 4;        // four strip images (80 KB)
 constexpr int kCgSmem = 2 * kCgStageBytes + kCgEpiBytes;      // 225 KB: two operand stages + staging
 #ifndef CG_EPI_WARPS
 #define CG_EPI_WARPS 12  // measured: 8 -> 0.808, 12 -> 0.772, 16 -> 0.804 ms at C3
@@ -436,10 +448,15 @@ __global__ void __launch_bounds__(kCgThreads, 1)
     } else {
         // ---------------------------------------------------------------- epilogue
         // warp w reads TMEM lane quarter q = w & 3 (rows i0 + 32 q + lane);
-        // the G warps of a quarter split its five 32-column chunks
+        // the G warps of a quarter split its five 32-column chunks and write
+        // the costs straight into the skewed image of strip s = 4 ib + q
+        // (stage[kk - j0][t] = d(32 s + t, kk - t): address 32 r + t, so a
+        // warp's stores hit 32 distinct banks); the image of rows
+        // [j0, rend) is contiguous in dsk and leaves with ONE bulk store
         constexpr int G = kCgEpiWarps / 4;  // warps per lane quarter
         const int q = warp & 3, hf = warp >> 2;
-        float *stage = reinterpret_cast<float *>(smem + 2 * kCgStageBytes) + q * 32 * kCgPitch;
+        float *stage = reinterpret_cast<float *>(smem + 2 * kCgStageBytes) + q * kCgStageRows * 32;
+        const bool leader = hf == 0 && lane == 0;  // issues the quarter's bulk store
         const float m2 = -2.0f * sc.inv;
         const int zb = (5 * hf) / G, ze = (5 * (hf + 1)) / G;  // this warp's 32-column chunks
         int li = 0;
@@ -451,6 +468,8 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             const int i = i0 + 32 * q + lane;
             const bool row_ok = i < N;
             const float xi = row_ok ? xn[(size_t)b * N + i] : 0.f;
+            const bool last = jb == JB - 1;
+            const int rows = (last ? KK : min(j0 + 128, KK)) - j0;  // skewed rows of this tile (<= 160)
             float yv[3];
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
@@ -459,8 +478,9 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             }
             tc::mbar_wait(&sh.acc_full[ab], (li >> 1) & 1);
             tc::tc_fence_after();
-            // the staging area is free once every epilogue warp finished the previous tile
-            named_bar_cg(1, 32 * kCgEpiWarps);
+            // the quarter's image is free once its previous bulk store has read it
+            if (leader) tc::bulk_wait_read0();
+            named_bar_cg(2 + q, 32 * G);
             const bool interior = j0 >= 32 && j0 + 128 <= M && bw == 0 && i0 + 128 <= N;
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
@@ -469,17 +489,22 @@ __global__ void __launch_bounds__(kCgThreads, 1)
                 float acc[32];
                 tc::tmem_ld32(tmem + 256u * ab + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * z), acc);
                 const int jz = j0 - 32 + 32 * z;
-                float *st = stage + lane * kCgPitch + 32 * z;
+                const int r0 = 32 * (z - 1) + lane;  // skewed row of element e: r0 + e
+                float *st = stage + r0 * 32 + lane;
                 if (interior) {
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) st[e] = tc_cost(acc[e], xi, __shfl_sync(kFull, yv[u], e), m2, true);
+                    for (int e = 0; e < 32; ++e) {
+                        const float v = tc_cost(acc[e], xi, __shfl_sync(kFull, yv[u], e), m2, true);
+                        if (r0 + e >= 0 && r0 + e < rows) st[e * 32] = v;
+                    }
                 } else {
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         const float yj = __shfl_sync(kFull, yv[u], e);
                         const int j = jz + e;
                         const bool ok = row_ok && j >= 0 && j < M && in_band(i + 1, j + 1, bw);
-                        st[e] = tc_cost(acc[e], xi, yj, m2, ok);
+                        const float v = tc_cost(acc[e], xi, yj, m2, ok);
+                        if (r0 + e >= 0 && r0 + e < rows) st[e * 32] = v;
                     }
                 }
             }
@@ -487,32 +512,17 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sh.acc_empty[ab]);
-            named_bar_cg(1, 32 * kCgEpiWarps);
+            // last column block: skewed rows past the computed columns
+            // (j = kk - t >= j0 + 128 >= M) are zero
+            if (hf == 0 && rows > 128)
+                for (int r = 128 + lane; r < rows; ++r) stage[r * 32 + lane] = 0.f;
+            tc::fence_async_smem();  // generic-proxy writes -> the bulk copy engine
+            named_bar_cg(2 + q, 32 * G);
             const int s = 4 * ib + q;
-            if (32 * s < N) {
-                float *ds = dsk + ((size_t)b * S + s) * (size_t)KK * 32;
-                const bool last = jb == JB - 1;
-                const int rend = last ? KK : min(j0 + 128, KK);
-                const int t4 = 4 * (lane & 7);
-                // the G warps of a lane quarter take interleaved groups of 4 rows
-                for (int kk0 = j0 + 4 * hf; kk0 < rend; kk0 += 4 * G) {
-                    const int kk = kk0 + (lane >> 3);
-                    const float *sr = stage + kk - j0 + 32;
-                    float v[4];
-                    if (!last) {
-#pragma unroll
-                        for (int c4 = 0; c4 < 4; ++c4) v[c4] = sr[(t4 + c4) * (kCgPitch - 1)];
-                    } else {
-#pragma unroll
-                        for (int c4 = 0; c4 < 4; ++c4) {
-                            const int lc = kk - (t4 + c4) - j0 + 32;
-                            v[c4] = lc < 160 ? stage[(t4 + c4) * kCgPitch + lc] : 0.f;
-                        }
-                    }
-                    *reinterpret_cast<float4 *>(ds + (size_t)kk * 32 + t4) = make_float4(v[0], v[1], v[2], v[3]);
-                }
-            }
+            if (leader && 32 * s < N)
+                tc::bulk_s2g(dsk + (((size_t)b * S + s) * (size_t)KK + j0) * 32, stage, (uint32_t)rows * 128u);
         }
+        if (leader) tc::bulk_wait0();
     }
     tc::tc_fence_before();
     __syncthreads();
