@@ -329,7 +329,8 @@ __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, i
 // ----------------------------------------------------------------------------
 // Unfused cost tensor on tcgen05 (materialize_costs, cost.hpp:82-99): one CTA
 // per (pair, 128-row block, 128-column block).  Operands come from the packed
-// fp16 hi/lo images by bulk copies (TMA engine), 64 features per round: A =
+// fp16 hi/lo images by bulk copies (TMA engine), 32 features per round and
+// four rounds in flight (a load warp and an MMA warp): A =
 // the 128 x rows, B = five 32-column y chunks [j0 - 32, j0 + 128) (N = 32
 // MMAs into TMEM columns 32 z).  The extra chunk on the left lets the CTA
 // write whole rows of the DP's skewed strip layout
@@ -341,17 +342,21 @@ __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, i
 // column block also writes the tail rows up to KK.
 // ----------------------------------------------------------------------------
 constexpr int kCgStageRows = 160;                             // skewed rows per strip image (KK - j0 <= 160)
-constexpr int kCgStageBytes = 32768 + 40960;                  // one round's operands: A 32 KB + B 40 KB
+constexpr int kCgKR = 32;                                     // features per operand round
+constexpr int kCgStages = 4;                                  // operand rounds in flight
+constexpr int kCgABytes = 128 * kCgKR * 2;                    // 128 x rows, one fp16 half (8 KB)
+constexpr int kCgBBytes = 160 * kCgKR * 2;                    // 160 y rows, one fp16 half (10 KB)
+constexpr int kCgStageBytes = 2 * kCgABytes + 2 * kCgBBytes;  // one round's operands: A hi|lo + B hi|lo (36 KB)
 constexpr int kCgEpiBytes = 4 * kCgStageRows * 32 * 4;        // four strip images (80 KB)
-constexpr int kCgSmem = 2 * kCgStageBytes + kCgEpiBytes;      // 225 KB: two operand stages + staging
+constexpr int kCgSmem = kCgStages * kCgStageBytes + kCgEpiBytes;  // 224 KB: four operand stages + staging
 #ifndef CG_EPI_WARPS
 #define CG_EPI_WARPS 12  // measured: 8 -> 0.808, 12 -> 0.772, 16 -> 0.804 ms at C3
 #endif
 constexpr int kCgEpiWarps = CG_EPI_WARPS;                     // epilogue warps (3 per TMEM lane quarter)
-constexpr int kCgThreads = 32 * (kCgEpiWarps + 1);            // + 1 producer warp
+constexpr int kCgThreads = 32 * (kCgEpiWarps + 2);            // + MMA warp + load warp
 
 struct CgShared {
-    uint64_t st_full[2], st_empty[2], acc_full[2], acc_empty[2];
+    uint64_t st_full[kCgStages], st_empty[kCgStages], acc_full[2], acc_empty[2];
     uint32_t tmem_base;
 };
 
@@ -369,12 +374,14 @@ __global__ void __launch_bounds__(kCgThreads, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NB = (N + 127) / 128, JB = (M + 127) / 128;
     const int ntiles = B * NB * JB;
-    const int rounds = dpad / 64;
+    const int rounds = dpad / kCgKR;
     const SplitScale sc = split_scale(absmax);
     if (tid == 0) {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kCgStages; ++k) {
             tc::mbar_init(&sh.st_full[k], 1);
             tc::mbar_init(&sh.st_empty[k], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
             tc::mbar_init(&sh.acc_full[k], 1);
             tc::mbar_init(&sh.acc_empty[k], kCgEpiWarps);
         }
@@ -392,47 +399,54 @@ __global__ void __launch_bounds__(kCgThreads, 1)
         b = r / NB;
     };
 
-    if (warp == kCgEpiWarps) {
-        // ---------------------------------------------------------------- producer
+    if (warp == kCgEpiWarps + 1) {
+        // ---------------------------------------------------------------- loads
+        // one bulk copy per operand half and round, kCgStages rounds ahead of
+        // the MMAs (the ring runs across tile boundaries)
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_f16_f32(128, 160);
-            int g = 0;  // global round counter of this CTA
-            auto issue_load = [&](int n, int kc, int gg) {
+            int g = 0;
+            for (int n = blockIdx.x; n < ntiles; n += gridDim.x) {
                 int b, ib, jb;
                 tile_of(n, b, ib, jb);
-                const int sb = gg & 1;
-                uint8_t *st = smem + sb * kCgStageBytes;
-                tc::mbar_wait(&sh.st_empty[sb], ((gg >> 1) & 1) ^ 1);
                 const uint8_t *xa = xp + ((size_t)b * NB + ib) * (size_t)128 * dpad * 4;
                 const uint8_t *ya = yp + ((size_t)b * JB + jb) * (size_t)160 * dpad * 4;
-                tc::mbar_expect_tx(&sh.st_full[sb], 32768u + 40960u);
-                tc::bulk_g2s(st, xa + (size_t)kc * 16384, 16384, &sh.st_full[sb]);
-                tc::bulk_g2s(st + 16384, xa + (size_t)128 * dpad * 2 + (size_t)kc * 16384, 16384, &sh.st_full[sb]);
-                tc::bulk_g2s(st + 32768, ya + (size_t)kc * 20480, 20480, &sh.st_full[sb]);
-                tc::bulk_g2s(st + 32768 + 20480, ya + (size_t)160 * dpad * 2 + (size_t)kc * 20480, 20480,
-                             &sh.st_full[sb]);
-            };
+                for (int kc = 0; kc < rounds; ++kc, ++g) {
+                    const int sb = g % kCgStages;
+                    uint8_t *st = smem + sb * kCgStageBytes;
+                    tc::mbar_wait(&sh.st_empty[sb], ((g / kCgStages) & 1) ^ 1);
+                    tc::mbar_expect_tx(&sh.st_full[sb], (uint32_t)kCgStageBytes);
+                    tc::bulk_g2s(st, xa + (size_t)kc * kCgABytes, kCgABytes, &sh.st_full[sb]);
+                    tc::bulk_g2s(st + kCgABytes, xa + (size_t)128 * dpad * 2 + (size_t)kc * kCgABytes, kCgABytes,
+                                 &sh.st_full[sb]);
+                    tc::bulk_g2s(st + 2 * kCgABytes, ya + (size_t)kc * kCgBBytes, kCgBBytes, &sh.st_full[sb]);
+                    tc::bulk_g2s(st + 2 * kCgABytes + kCgBBytes, ya + (size_t)160 * dpad * 2 + (size_t)kc * kCgBBytes,
+                                 kCgBBytes, &sh.st_full[sb]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kCgEpiWarps) {
+        // ---------------------------------------------------------------- MMA
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_f16_f32(128, 160);
+            int g = 0;   // global round counter of this CTA
             int li = 0;  // local tile index
-            const int first = blockIdx.x;
-            if (first < ntiles) issue_load(first, 0, 0);
-            for (int n = first; n < ntiles; n += gridDim.x, ++li) {
+            for (int n = blockIdx.x; n < ntiles; n += gridDim.x, ++li) {
                 const int ab = li & 1;
                 tc::mbar_wait(&sh.acc_empty[ab], ((li >> 1) & 1) ^ 1);  // epilogue done with tile li - 2
                 tc::tc_fence_after();
                 for (int kc = 0; kc < rounds; ++kc, ++g) {
-                    // prefetch the next round (this tile's or the next tile's first)
-                    if (kc + 1 < rounds) issue_load(n, kc + 1, g + 1);
-                    else if (n + (int)gridDim.x < ntiles) issue_load(n + gridDim.x, 0, g + 1);
-                    const int sb = g & 1;
-                    tc::mbar_wait(&sh.st_full[sb], (g >> 1) & 1);
+                    const int sb = g % kCgStages;
+                    tc::mbar_wait(&sh.st_full[sb], (g / kCgStages) & 1);
                     tc::tc_fence_after();
                     // one M = 128, N = 160 MMA per K step and pass: B = the
                     // 160 y rows [j0 - 32, j0 + 128) (K-block stride 2560 B)
-                    const uint32_t ah = tc::smem_u32(smem + sb * kCgStageBytes), al = ah + 16384;
-                    const uint32_t bh = ah + 32768, bl = bh + 20480;
+                    const uint32_t ah = tc::smem_u32(smem + sb * kCgStageBytes), al = ah + kCgABytes;
+                    const uint32_t bh = ah + 2 * kCgABytes, bl = bh + kCgBBytes;
                     const uint32_t d = tmem + 256u * ab;
-                    for (int ks = 0; ks < 4; ++ks) {
-                        const int kg = 4 * kc + ks;
+#pragma unroll
+                    for (int ks = 0; ks < kCgKR / 16; ++ks) {
+                        const int kg = (kCgKR / 16) * kc + ks;
                         const uint32_t oa = ks * 4096, ob = ks * 5120;
                         const uint32_t acc0 = kg > 0 ? 1u : 0u;
                         tc::mma_f16(d, tc::smem_desc(ah + oa, 2048, 128), tc::smem_desc(bh + ob, 2560, 128), idesc, acc0);
@@ -455,7 +469,7 @@ __global__ void __launch_bounds__(kCgThreads, 1)
         // [j0, rend) is contiguous in dsk and leaves with ONE bulk store
         constexpr int G = kCgEpiWarps / 4;  // warps per lane quarter
         const int q = warp & 3, hf = warp >> 2;
-        float *stage = reinterpret_cast<float *>(smem + 2 * kCgStageBytes) + q * kCgStageRows * 32;
+        float *stage = reinterpret_cast<float *>(smem + kCgStages * kCgStageBytes) + q * kCgStageRows * 32;
         const bool leader = hf == 0 && lane == 0;  // issues the quarter's bulk store
         const float m2 = -2.0f * sc.inv;
         const int zb = (5 * hf) / G, ze = (5 * (hf + 1)) / G;  // this warp's 32-column chunks
