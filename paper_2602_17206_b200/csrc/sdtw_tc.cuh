@@ -347,6 +347,9 @@ constexpr int kCgStages = 4;                                  // operand rounds 
 constexpr int kCgABytes = 128 * kCgKR * 2;                    // 128 x rows, one fp16 half (8 KB)
 constexpr int kCgBBytes = 160 * kCgKR * 2;                    // 160 y rows, one fp16 half (10 KB)
 constexpr int kCgStageBytes = 2 * kCgABytes + 2 * kCgBBytes;  // one round's operands: A hi|lo + B hi|lo (36 KB)
+constexpr int kCgXHalf = 128 * 128 * 2;                       // resident x rows, one fp16 half (dpad <= 128)
+static_assert(2 * kCgXHalf + kCgStages * 2 * kCgBBytes <= kCgStages * kCgStageBytes,
+              "resident x + the y ring must fit the operand ring");
 constexpr int kCgEpiBytes = 4 * kCgStageRows * 32 * 4;        // four strip images (80 KB)
 constexpr int kCgSmem = kCgStages * kCgStageBytes + kCgEpiBytes;  // 224 KB: four operand stages + staging
 #ifndef CG_EPI_WARPS
@@ -356,7 +359,7 @@ constexpr int kCgEpiWarps = CG_EPI_WARPS;                     // epilogue warps 
 constexpr int kCgThreads = 32 * (kCgEpiWarps + 2);            // + MMA warp + load warp
 
 struct CgShared {
-    uint64_t st_full[kCgStages], st_empty[kCgStages], acc_full[2], acc_empty[2];
+    uint64_t st_full[kCgStages], st_empty[kCgStages], acc_full[2], acc_empty[2], x_full, x_empty;
     uint32_t tmem_base;
 };
 
@@ -381,6 +384,8 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             tc::mbar_init(&sh.st_full[k], 1);
             tc::mbar_init(&sh.st_empty[k], 1);
         }
+        tc::mbar_init(&sh.x_full, 1);
+        tc::mbar_init(&sh.x_empty, 1);
         for (int k = 0; k < 2; ++k) {
             tc::mbar_init(&sh.acc_full[k], 1);
             tc::mbar_init(&sh.acc_empty[k], kCgEpiWarps);
@@ -392,6 +397,12 @@ __global__ void __launch_bounds__(kCgThreads, 1)
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = sh.tmem_base;
+    // a contiguous range of tiles per CTA (jb fastest): consecutive tiles
+    // share the 128 x rows, which stay resident in shared memory when
+    // dpad <= 128 (xres; the ring then carries y only)
+    const int t0 = (int)((long long)blockIdx.x * ntiles / gridDim.x);
+    const int t1 = (int)((long long)(blockIdx.x + 1) * ntiles / gridDim.x);
+    const bool xres = dpad <= 128;
     auto tile_of = [&](int n, int &b, int &ib, int &jb) {
         jb = n % JB;
         const int r = n / JB;
@@ -404,16 +415,33 @@ __global__ void __launch_bounds__(kCgThreads, 1)
         // one bulk copy per operand half and round, kCgStages rounds ahead of
         // the MMAs (the ring runs across tile boundaries)
         if (lane == 0) {
-            int g = 0;
-            for (int n = blockIdx.x; n < ntiles; n += gridDim.x) {
+            int g = 0, xr = 0;
+            for (int n = t0; n < t1; ++n) {
                 int b, ib, jb;
                 tile_of(n, b, ib, jb);
                 const uint8_t *xa = xp + ((size_t)b * NB + ib) * (size_t)128 * dpad * 4;
                 const uint8_t *ya = yp + ((size_t)b * JB + jb) * (size_t)160 * dpad * 4;
+                if (xres && (n == t0 || n / JB != (n - 1) / JB)) {
+                    // new x rows: wait until the MMAs on the previous ones are done
+                    if (xr > 0) tc::mbar_wait(&sh.x_empty, (xr - 1) & 1);
+                    const uint32_t xb = 128u * dpad * 2;
+                    tc::mbar_expect_tx(&sh.x_full, 2 * xb);
+                    tc::bulk_g2s(smem, xa, xb, &sh.x_full);
+                    tc::bulk_g2s(smem + kCgXHalf, xa + xb, xb, &sh.x_full);
+                    ++xr;
+                }
                 for (int kc = 0; kc < rounds; ++kc, ++g) {
                     const int sb = g % kCgStages;
-                    uint8_t *st = smem + sb * kCgStageBytes;
                     tc::mbar_wait(&sh.st_empty[sb], ((g / kCgStages) & 1) ^ 1);
+                    if (xres) {
+                        uint8_t *st = smem + 2 * kCgXHalf + sb * 2 * kCgBBytes;
+                        tc::mbar_expect_tx(&sh.st_full[sb], 2u * kCgBBytes);
+                        tc::bulk_g2s(st, ya + (size_t)kc * kCgBBytes, kCgBBytes, &sh.st_full[sb]);
+                        tc::bulk_g2s(st + kCgBBytes, ya + (size_t)160 * dpad * 2 + (size_t)kc * kCgBBytes, kCgBBytes,
+                                     &sh.st_full[sb]);
+                        continue;
+                    }
+                    uint8_t *st = smem + sb * kCgStageBytes;
                     tc::mbar_expect_tx(&sh.st_full[sb], (uint32_t)kCgStageBytes);
                     tc::bulk_g2s(st, xa + (size_t)kc * kCgABytes, kCgABytes, &sh.st_full[sb]);
                     tc::bulk_g2s(st + kCgABytes, xa + (size_t)128 * dpad * 2 + (size_t)kc * kCgABytes, kCgABytes,
@@ -431,18 +459,33 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             const uint32_t idesc = tc::idesc_f16_f32(128, 160);
             int g = 0;   // global round counter of this CTA
             int li = 0;  // local tile index
-            for (int n = blockIdx.x; n < ntiles; n += gridDim.x, ++li) {
+            int xm = 0;  // x blocks consumed
+            for (int n = t0; n < t1; ++n, ++li) {
                 const int ab = li & 1;
                 tc::mbar_wait(&sh.acc_empty[ab], ((li >> 1) & 1) ^ 1);  // epilogue done with tile li - 2
                 tc::tc_fence_after();
+                if (xres && (n == t0 || n / JB != (n - 1) / JB)) {
+                    tc::mbar_wait(&sh.x_full, xm & 1);
+                    tc::tc_fence_after();
+                    ++xm;
+                }
                 for (int kc = 0; kc < rounds; ++kc, ++g) {
                     const int sb = g % kCgStages;
                     tc::mbar_wait(&sh.st_full[sb], (g / kCgStages) & 1);
                     tc::tc_fence_after();
                     // one M = 128, N = 160 MMA per K step and pass: B = the
                     // 160 y rows [j0 - 32, j0 + 128) (K-block stride 2560 B)
-                    const uint32_t ah = tc::smem_u32(smem + sb * kCgStageBytes), al = ah + kCgABytes;
-                    const uint32_t bh = ah + 2 * kCgABytes, bl = bh + kCgBBytes;
+                    uint32_t ah, al, bh;
+                    if (xres) {
+                        ah = tc::smem_u32(smem) + kc * kCgABytes;
+                        al = ah + kCgXHalf;
+                        bh = tc::smem_u32(smem + 2 * kCgXHalf + sb * 2 * kCgBBytes);
+                    } else {
+                        ah = tc::smem_u32(smem + sb * kCgStageBytes);
+                        al = ah + kCgABytes;
+                        bh = ah + 2 * kCgABytes;
+                    }
+                    const uint32_t bl = bh + kCgBBytes;
                     const uint32_t d = tmem + 256u * ab;
 #pragma unroll
                     for (int ks = 0; ks < kCgKR / 16; ++ks) {
@@ -456,6 +499,8 @@ __global__ void __launch_bounds__(kCgThreads, 1)
                     tc::mma_commit(&sh.st_empty[sb]);  // the stage is free once these MMAs finish
                 }
                 tc::mma_commit(&sh.acc_full[ab]);
+                // last tile on these x rows: they may be replaced once its MMAs finish
+                if (xres && n + 1 < t1 && (n + 1) / JB != n / JB) tc::mma_commit(&sh.x_empty);
             }
         }
         __syncwarp();
@@ -474,7 +519,7 @@ __global__ void __launch_bounds__(kCgThreads, 1)
         const float m2 = -2.0f * sc.inv;
         const int zb = (5 * hf) / G, ze = (5 * (hf + 1)) / G;  // this warp's 32-column chunks
         int li = 0;
-        for (int n = blockIdx.x; n < ntiles; n += gridDim.x, ++li) {
+        for (int n = t0; n < t1; ++n, ++li) {
             int b, ib, jb;
             tile_of(n, b, ib, jb);
             const int i0 = 128 * ib, j0 = 128 * jb;
