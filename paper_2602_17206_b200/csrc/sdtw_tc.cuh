@@ -135,6 +135,20 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// the same with an L2 eviction-priority hint (createpolicy)
+__device__ __forceinline__ void bulk_s2g_hint(void *dst, const void *src, uint32_t bytes, uint64_t policy)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes), "l"(policy)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 // the thread's bulk stores have finished reading shared memory
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // the thread's bulk stores are complete
@@ -516,6 +530,8 @@ __global__ void __launch_bounds__(kCgThreads, 1)
         const int q = warp & 3, hf = warp >> 2;
         float *stage = reinterpret_cast<float *>(smem + kCgStages * kCgStageBytes) + q * kCgStageRows * 32;
         const bool leader = hf == 0 && lane == 0;  // issues the quarter's bulk store
+        // the cost stream must not push the operands (re-read per tile row) out of L2
+        const uint64_t st_policy = tc::l2_evict_first_policy();
         const float m2 = -2.0f * sc.inv;
         const int zb = (5 * hf) / G, ze = (5 * (hf + 1)) / G;  // this warp's 32-column chunks
         int li = 0;
@@ -579,7 +595,8 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             named_bar_cg(2 + q, 32 * G);
             const int s = 4 * ib + q;
             if (leader && 32 * s < N)
-                tc::bulk_s2g(dsk + (((size_t)b * S + s) * (size_t)KK + j0) * 32, stage, (uint32_t)rows * 128u);
+                tc::bulk_s2g_hint(dsk + (((size_t)b * S + s) * (size_t)KK + j0) * 32, stage, (uint32_t)rows * 128u,
+                                  st_policy);
         }
         if (leader) tc::bulk_wait0();
     }
