@@ -803,7 +803,10 @@ size_t e2e_chunks(sdtw_ctx *ctx, size_t B, size_t N, size_t M, size_t D, int ptr
     // (measured, scripts/e2e_timeline.py: C2 2.26 -> 2.02 ms, C3 no gain)
     const size_t strips = B * ((N + 31) / 32);
     if (strips > (size_t)ctx->sm_count * 8) return 1;
-    return std::min<size_t>(4, B);
+    // copy-dominated calls (wide features) pipeline finer: C4 (D = 1024,
+    // 134 MB over PCIe vs 0.43 ms of device work) 2.20 -> 2.01 ms with 8
+    // chunks; C2 is best at 4 (1.98 vs 2.08 ms with 8)
+    return std::min<size_t>(D >= 512 ? 8 : 4, B);
 }
 
 template <class T>
