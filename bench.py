@@ -6,13 +6,17 @@ L, D; peak HBM MB; 1/2/4/8 GPU.  cells/s = B*N*M / t(fwd+bwd), where one
 step = loss + grad_x + grad_y of the whole batch (sdtw_with_gradients,
 backward.hpp:276-304).
 
-Default workload = BASELINE.json configs[1]: B=32, N=M=1024, D=128,
-gamma=0.1, UNFUSED (the headline `value`), with the FUSED mode of the same
-config measured in the same run (`fused`).  `--config c3` runs the
-north-star case (L=4096, gamma=0.01; use --mode fused for its fused target),
-`--config c5` the Soft-DTW barycenter (B=1024 members, L=512, D=64): one
-step = objective + gradient over all members + NCCL allreduce of grad_z
-across ranks + Adam update (members sharded over ranks: strong scaling).
+Default workload = the north-star config, BASELINE.json configs[2]: B=32,
+N=M=4096, D=128, gamma=0.01, FUSED (the headline `value`; the largest
+single-GPU config and the one `north_star`'s target is stated on), with the
+UNFUSED mode of the same config measured in the same run (`unfused`).
+Inputs on both arms are the reference's own bench generator (bench.hpp:61-66:
+N(0,1) from mt19937_64(42), all of x then all of y), so the data-dependent
+zero-tile skipping sees the same data the reference arm times.
+`--config c1|c2|c4` run the other pair configs, `--config c5` the Soft-DTW
+barycenter (B=1024 members, L=512, D=64): one step = objective + gradient
+over all members + NCCL allreduce of grad_z across ranks + Adam update
+(members sharded over ranks: strong scaling).
 
 Arms:
   (default)         this engine (libsdtw_b200.so through the C-ABI).
@@ -22,7 +26,9 @@ Arms:
 
 Multi-GPU: launched by torchrun, one rank per GPU; pairs are independent so
 every rank runs its own B=32 batch with no collective on the data path
-(weak scaling); time = max over ranks of the device-timed region.
+(weak scaling, `value`); the same run also times ONE B=32 batch split into
+contiguous B/N pair shards (`strong_b32`, pairs/s); time =
+max over ranks of the device-timed region.
 """
 from __future__ import annotations
 
@@ -173,6 +179,20 @@ def cpu_reference_rate(cfg, fused, threads, reps, warmup, max_pairs=None):
               f"L={cfg['L']} D={cfg['D']} gamma={cfg['gamma']}, {reps} timed reps after "
               f"{warmup} warm-up, threads={threads}")
     return cells / (mean_ms / 1e3), mean_ms, sample
+
+
+def bench_inputs(B, L, D, seed):
+    """The reference's own generator (bench.hpp:61-66) through
+    oracle/_ref/libsdtw_ref.so: the engine arm's inputs equal the reference
+    arm's.  Falls back to numpy N(0,1) only if that library is absent."""
+    import numpy as np
+    try:
+        import oracle
+        return oracle.Reference().bench_inputs(B, L, D, seed=seed)
+    except Exception:
+        rng = np.random.default_rng(seed)
+        return (rng.standard_normal((B, L, D), dtype=np.float32),
+                rng.standard_normal((B, L, D), dtype=np.float32))
 
 
 def _ref_pairs_for(cfg):
@@ -441,9 +461,9 @@ def run_engine_arm(args, cfg):
     torch.cuda.set_stream(side)
     eng.set_stream(side.cuda_stream)
     B, L, D, gamma = cfg["B"], cfg["L"], cfg["D"], cfg["gamma"]
-    gen = torch.Generator(device="cuda").manual_seed(42 + rank)
-    x = torch.randn((B, L, D), generator=gen, device="cuda", dtype=torch.float32)
-    y = torch.randn((B, L, D), generator=gen, device="cuda", dtype=torch.float32)
+    xh_np, yh_np = bench_inputs(B, L, D, 42 + rank)
+    x = torch.from_numpy(xh_np).cuda()
+    y = torch.from_numpy(yh_np).cuda()
     outs = (torch.empty(B, device="cuda"), torch.empty((B, L, D), device="cuda"),
             torch.empty((B, L, D), device="cuda"))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -480,6 +500,25 @@ def run_engine_arm(args, cfg):
                  "value": cells_per_rank * ws * args.steps / (o_max / 1e3), "unit": "cells/s",
                  "ms_per_step": o_max / args.steps, "peak_hbm_mb": o_peak / 2**20,
                  "phase_ms_per_step": {k: v / args.steps for k, v in o_ph.items()}}
+
+    # ---- strong scaling of ONE B=32 batch: contiguous
+    # B/N pair shards, no collective; max-over-ranks device time ----------
+    strong = None
+    if ws > 1:
+        from paper_2602_17206_b200.sharding import shard_range
+        b0, b1 = shard_range(B, ws, rank)
+        xs_, ys_ = x[b0:b1].contiguous(), y[b0:b1].contiguous()
+        outs_s = (outs[0][b0:b1], outs[1][b0:b1], outs[2][b0:b1])
+        dist.barrier()
+        s_ms, _, _, _ = time_engine(eng, torch, xs_, ys_, outs_s, fused, gamma, args.steps,
+                                    min(args.warmup, 3), flush)
+        ts = torch.tensor([s_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        s_max = float(ts.item())
+        strong = {"batch": B, "pairs_per_gpu": f"{b1 - b0} (contiguous shard of one B={B} batch)",
+                  "pairs_per_s": B * args.steps / (s_max / 1e3),
+                  "cells_per_s": B * L * L * args.steps / (s_max / 1e3),
+                  "ms_per_step": s_max / args.steps}
 
     # ---- e2e through the public API with pinned host buffers ----------
     xh = x.cpu().pin_memory()
@@ -558,7 +597,8 @@ def run_engine_arm(args, cfg):
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic N(0,1) (torch.randn, seed 42+rank), fp32",
+            "data": "synthetic N(0,1) from the reference's bench generator (bench.hpp:61-66, "
+                    "mt19937_64 seed 42+rank, x then y), fp32",
             "config": _config_dict(args, cfg, ws),
             "peak_hbm_mb": peak / 2**20,
             "phase_ms_per_step": per_step,
@@ -568,7 +608,10 @@ def run_engine_arm(args, cfg):
             "gpu_launches": launches,
             "roofline": roofline,
             "clocks": clk,
+            "pairs_per_s": B * ws * args.steps / (max_ms / 1e3),
         }
+        if strong:
+            line["strong_b32"] = strong
         if other:
             line["unfused" if fused else "fused"] = other
         if ws == 1 and not args.no_cpu_baseline:
@@ -606,8 +649,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--mode", default="unfused", choices=["fused", "unfused"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="fused", choices=["fused", "unfused"])
     ap.add_argument("--single-mode", action="store_true", help="skip the other cost mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

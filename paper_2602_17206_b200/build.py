@@ -24,6 +24,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
+    "--split-compile=0",
 ]
 
 

@@ -66,6 +66,12 @@ struct Allocator {
 
     static size_t round(size_t b) { return b < 512 ? 512 : (b + 511) & ~size_t(511); }
 
+    // called when cudaMalloc fails after this cache was trimmed: releases the
+    // cached blocks of the other allocators on the device (parent context and
+    // its pair-chunk sub-contexts) before the call gives up
+    void (*on_oom)(void *) = nullptr;
+    void *on_oom_arg = nullptr;
+
     void *alloc(size_t bytes)
     {
         const size_t sz = round(bytes);
@@ -79,6 +85,10 @@ struct Allocator {
             if (cudaMalloc(&p, sz) != cudaSuccess) {
                 cudaGetLastError();
                 trim();
+                if (on_oom && cudaMalloc(&p, sz) != cudaSuccess) {
+                    cudaGetLastError();
+                    on_oom(on_oom_arg);
+                }
                 if (cudaMalloc(&p, sz) != cudaSuccess) {
                     cudaGetLastError();
                     fail(SDTW_ENOMEM, "cudaMalloc failed", sz);
@@ -104,7 +114,35 @@ struct Allocator {
         for (auto &kv : cache) cudaFree(kv.second);
         cache.clear();
     }
+    // frees a live block at once (not into the cache): the persistent halo
+    // arena when it has to grow
+    void free_now(void *p)
+    {
+        if (!p) return;
+        auto it = live.find(p);
+        if (it == live.end()) return;
+        live_bytes -= it->second;
+        live.erase(it);
+        cudaFree(p);
+    }
 };
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: kept
+// per (device, kernel) and only ever raised, so concurrent contexts on one
+// device cannot lower the limit under each other's launches.
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void *>, int> g_attr;
+void ensure_smem_attr(int device, const void *kern, int bytes)
+{
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int &cur = g_attr[{device, kern}];
+    if (cur >= bytes) return;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        fail(SDTW_ECUDA, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+    }
+    cur = bytes;
+}
 
 // dlopen'ed NCCL (shares the process's libnccl.so.2, e.g. torch's copy).
 struct Nccl {
@@ -149,6 +187,7 @@ struct sdtw_ctx {
     // the epoch of the call that wrote them, so no per-call clearing).
     void *halo_arena = nullptr;
     size_t halo_bytes = 0;
+    unsigned long long halo_sig[5] = {};
     unsigned epoch = 0;
     unsigned long long *trace = nullptr;  // debug: per-strip forward timestamps
     cudaEvent_t ev[SDTW_NUM_PHASES][2] = {};
@@ -157,6 +196,7 @@ struct sdtw_ctx {
     // sub-context (stream, stream-ordered allocator, halo arena), so the
     // host<->device copies of one chunk overlap the DP of the others.
     std::vector<sdtw_ctx *> subs;
+    sdtw_ctx *parent = nullptr;
     cudaEvent_t fork_ev = nullptr;
     std::vector<cudaEvent_t> join_ev;
 };
@@ -407,20 +447,22 @@ struct Pipeline {
     {
         reset_phases(ctx);
         Phase ph(ctx, 0);
-        absmax = Buf<unsigned>(ctx, 2);
-        CUDA_OK(cudaMemsetAsync(absmax.p, 0, 2 * sizeof(unsigned), ctx->stream));
+        // per-pair operand maxima [2 b] (x), [2 b + 1] (y): a pair's split
+        // scale, costs and fixed-point scales depend on that pair alone
+        absmax = Buf<unsigned>(ctx, 2 * (size_t)B);
+        CUDA_OK(cudaMemsetAsync(absmax.p, 0, 2 * (size_t)B * sizeof(unsigned), ctx->stream));
         xn = Buf<T>(ctx, (size_t)B * N);
         yn = Buf<T>(ctx, (size_t)B * M);
         if constexpr (std::is_same<T, float>::value) {
-            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * N + 7) / 8), 256, 0, x, B * N, D, xn.p,
-                   absmax.p);
-            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * M + 7) / 8), 256, 0, y, B * M, D, yn.p,
-                   absmax.p + 1);
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * N + 7) / 8), 256, 0, x,
+                   B * N, D, xn.p, absmax.p, N, 0);
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * M + 7) / 8), 256, 0, y,
+                   B * M, D, yn.p, absmax.p, M, 1);
         } else {
-            LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * N * D, 256, 1024), 256, 0, x,
-                   (size_t)B * N * D, absmax.p);
-            LAUNCH(ctx, sdtw::absmax_any_kernel<T>, grid_for((size_t)B * M * D, 256, 1024), 256, 0, y,
-                   (size_t)B * M * D, absmax.p + 1);
+            LAUNCH(ctx, sdtw::absmax_any_kernel<T>, dim3(grid_for((size_t)N * D, 256, 64), (unsigned)B), 256, 0, x,
+                   (size_t)N * D, absmax.p, 0);
+            LAUNCH(ctx, sdtw::absmax_any_kernel<T>, dim3(grid_for((size_t)M * D, 256, 64), (unsigned)B), 256, 0, y,
+                   (size_t)M * D, absmax.p, 1);
             LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * N, 128), 128, 0, x, B * N, D, xn.p);
             LAUNCH(ctx, sdtw::norms_kernel<T>, grid_for((size_t)B * M, 128), 128, 0, y, B * M, D, yn.p);
         }
@@ -433,12 +475,7 @@ struct Pipeline {
         const size_t total = (size_t)B * S * KK * 32;
         dsk = Buf<T>(ctx, total);
         if constexpr (std::is_same<T, float>::value) {
-            static bool attr = false;
-            if (!attr) {
-                CUDA_OK(cudaFuncSetAttribute(sdtw::cost_gemm_tc_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, sdtw::kCgSmem));
-                attr = true;
-            }
+            ensure_smem_attr(ctx->device, (const void *)sdtw::cost_gemm_tc_kernel, sdtw::kCgSmem);
             // operands packed once (fp16 hi/lo core-matrix images), then
             // bulk-copied by every CTA that needs them
             const int NB = (N + 127) / 128;
@@ -465,20 +502,8 @@ struct Pipeline {
     unsigned persistent_grid(Kern kern, int threads, size_t smem, int work_warps)
     {
         int occ = 0;
-        CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_smem_attr(ctx->device, (const void *)kern, (int)smem);
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-        if (std::getenv("SDTW_DEBUG_OCC")) {
-            std::fprintf(stderr, "[sdtw] occupancy %d blocks/SM (threads %d, smem %zu)\n", occ, threads, smem);
-            cudaFuncAttributes fa{};
-            cudaFuncGetAttributes(&fa, kern);
-            std::fprintf(stderr, "[sdtw]   regs %d static smem %zu local %zu maxthreads %d\n", fa.numRegs,
-                         fa.sharedSizeBytes, fa.localSizeBytes, fa.maxThreadsPerBlock);
-            for (size_t kb = 90; kb <= 114; kb += 4) {
-                int o = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, kb * 1024);
-                std::fprintf(stderr, "[sdtw]   %zu KB -> %d\n", kb, o);
-            }
-        }
         if (occ < 1) fail(SDTW_ECUDA, "DP kernel does not fit on an SM");
         const int wpc = threads / 32;
         const int need = (work_warps + wpc - 1) / wpc;
@@ -496,22 +521,33 @@ struct Pipeline {
     int tile_quota = 0;
     Buf<unsigned> stats;
 
+    // The tagged-halo arena persists across calls (entries carry the epoch of
+    // the call that wrote them, so no per-call clearing).  It is allocated
+    // through the context allocator (it counts in sdtw_mem_stats and against
+    // sdtw_set_mem_limit) and zeroed whenever it grows, the entry layout
+    // (dtype, B, S, M, C) changes or the epoch wraps, so a stale word of a
+    // differently shaped call can never carry the current epoch.
     void halos()
     {
         const size_t need = 2 * (size_t)B * S * M * sizeof(Ent) + (size_t)B * S * C * 8;
+        const unsigned long long sig[5] = {sizeof(T), (unsigned long long)B, (unsigned long long)S,
+                                           (unsigned long long)M, (unsigned long long)C};
+        bool zero = false;
         if (ctx->halo_bytes < need) {
             if (ctx->halo_arena) {
                 CUDA_OK(cudaStreamSynchronize(ctx->stream));
-                cudaFree(ctx->halo_arena);
+                ctx->alloc.free_now(ctx->halo_arena);
                 ctx->halo_arena = nullptr;
                 ctx->halo_bytes = 0;
             }
-            if (cudaMalloc(&ctx->halo_arena, need) != cudaSuccess) {
-                cudaGetLastError();
-                fail(SDTW_ENOMEM, "cudaMalloc failed (halo arena)", need);
-            }
-            CUDA_OK(cudaMemsetAsync(ctx->halo_arena, 0, need, ctx->stream));
+            ctx->halo_arena = ctx->alloc.alloc(need);
             ctx->halo_bytes = need;
+            zero = true;
+        }
+        if (std::memcmp(sig, ctx->halo_sig, sizeof sig) != 0 || ctx->epoch >= 0xfffffff0u) zero = true;
+        if (zero) {
+            CUDA_OK(cudaMemsetAsync(ctx->halo_arena, 0, need, ctx->stream));
+            std::memcpy(ctx->halo_sig, sig, sizeof sig);
             ctx->epoch = 0;
         }
         hbt = static_cast<Ent *>(ctx->halo_arena);
@@ -576,21 +612,12 @@ struct Pipeline {
             if constexpr (std::is_same<T, float>::value) {
                 auto A = args3();
                 const size_t smem = 2 * sdtw::ftc_slot_bytes(dpad);
-                static size_t attr = 0;
-                if (attr != smem) {
-                    CUDA_OK(cudaFuncSetAttribute(sdtw::sdtw_forward_tc_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    attr = smem;
-                }
+                ensure_smem_attr(ctx->device, (const void *)sdtw::sdtw_forward_tc_kernel,
+                                 (int)(2 * sdtw::ftc_slot_bytes(sdtw::kFtcMaxD)));
                 const int work = B * ((S + 3) / 4);
                 const unsigned grid = (unsigned)std::max(1, std::min((work + 1) / 2, ctx->sm_count));
                 LAUNCH(ctx, sdtw::sdtw_forward_tc_kernel, grid, sdtw::kFtcThreads, smem, A, ftc());
             }
-        } else if (const char *e = std::getenv("SDTW_DEBUG_FWD_K")) {  // experiment hook
-            const int k = std::atoi(e);
-            if (k >= 4) launch_forward3<4>();
-            else if (k == 2) launch_forward3<2>();
-            else launch_forward3<1>();
         } else if (!fused) {
             // one strip per warp: the lean step body (K == 1) beats strip ILP
             // at every config measured (C5, 16384 strips: K=1 5.78 ms per Adam
@@ -764,6 +791,17 @@ void fwd_bwd_run(sdtw_ctx *c, const T *x, const T *y, size_t B, size_t N, size_t
     gyo.finish(c);
 }
 
+// On a failed cudaMalloc inside a sub-context: synchronise and release the
+// cached (free) blocks of the parent and of every sibling sub-context.
+void trim_family(void *arg)
+{
+    sdtw_ctx *c = static_cast<sdtw_ctx *>(arg);
+    sdtw_ctx *root = c->parent ? c->parent : c;
+    cudaDeviceSynchronize();
+    root->alloc.trim();
+    for (auto *sc : root->subs) sc->alloc.trim();
+}
+
 sdtw_ctx *sub_context(sdtw_ctx *ctx, size_t i)
 {
     while (ctx->subs.size() <= i) {
@@ -775,6 +813,9 @@ sdtw_ctx *sub_context(sdtw_ctx *ctx, size_t i)
             fail(SDTW_ECUDA, "cudaStreamCreate failed (sub-context)");
         }
         c->stream = c->own_stream;
+        c->parent = ctx;
+        c->alloc.on_oom = trim_family;
+        c->alloc.on_oom_arg = c;
         ctx->subs.push_back(c);
         cudaEvent_t e;
         CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1138,6 +1179,8 @@ int sdtw_ctx_create(int device, sdtw_ctx **out)
             return SDTW_ECUDA;
         }
         ctx->sm_count = prop.multiProcessorCount;
+        ctx->alloc.on_oom = trim_family;
+        ctx->alloc.on_oom_arg = ctx;
         CUDA_OK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
         ctx->stream = ctx->own_stream;
         *out = ctx;
@@ -1158,7 +1201,6 @@ int sdtw_ctx_destroy(sdtw_ctx *ctx)
         for (auto *sc : ctx->subs) {
             cudaStreamSynchronize(sc->stream);
             for (auto &kv : sc->alloc.live) cudaFree(kv.first);
-            if (sc->halo_arena) cudaFree(sc->halo_arena);
             sc->alloc.trim();
             if (sc->own_stream) cudaStreamDestroy(sc->own_stream);
             delete sc;
@@ -1166,7 +1208,6 @@ int sdtw_ctx_destroy(sdtw_ctx *ctx)
         for (auto e : ctx->join_ev) cudaEventDestroy(e);
         if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
         for (auto &kv : ctx->alloc.live) cudaFree(kv.first);
-        if (ctx->halo_arena) cudaFree(ctx->halo_arena);
         ctx->alloc.trim();
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     }

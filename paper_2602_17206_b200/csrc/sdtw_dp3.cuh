@@ -87,7 +87,10 @@ struct Tagged<double> {
     {
         unsigned long long t;
         asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(t) : "l"(&p->tag) : "memory");
-        if ((unsigned)t != tag) return false;
+        // the whole word: genuine fp64 tags have a zero high word, while fp32
+        // entries and backward status words left by earlier calls carry an
+        // epoch >= 1 there (the arena is shared across calls and dtypes)
+        if (t != (unsigned long long)tag) return false;
         __threadfence();
         asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(&p->v) : "memory");
         return true;
@@ -111,7 +114,7 @@ struct Dp3Args {
     // acceptance.cpp:348-377).  value = acc * 2^-fx_*.
     long long *gx_fx, *gy_fx;      // [B][N][D] sum_j E y_j,  [B][M][D] sum_i E x_i
     long long *rs_fx, *cs_fx;      // [B][N] row marginals, [B][M] column marginals
-    const unsigned *absmax;        // [0] max|x|, [1] max|y| (fp32 bit patterns)
+    const unsigned *absmax;        // [2 b] max|x|, [2 b + 1] max|y| of pair b (fp32 bit patterns)
     // compact store of non-zero E tiles for the contraction (sdtw_grad.cuh):
     // strip (b, s) owns slots [(b S + s) quota, +quota), filled in its
     // processing order (chunks right to left); tiles past the quota are
@@ -157,15 +160,17 @@ __device__ __forceinline__ void fx_add(long long *p, double v, double scale)
     if (q != 0) atomicAdd(reinterpret_cast<unsigned long long *>(p), (unsigned long long)q);
 }
 
-// Absolute maxima for the fixed-point scales (works for float and double).
+// Per-pair absolute maxima for the fixed-point scales (float and double):
+// pair b = blockIdx.y, n elements per pair, into out[2 b + which].
 template <class T>
-__global__ void absmax_any_kernel(const T *__restrict__ v, size_t n, unsigned *out)
+__global__ void absmax_any_kernel(const T *__restrict__ v, size_t n, unsigned *out, int which)
 {
+    const T *p = v + (size_t)blockIdx.y * n;
     float m = 0.f;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        m = fmaxf(m, (float)fabs((double)v[i]));
+        m = fmaxf(m, (float)fabs((double)p[i]));
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, off));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m) + 1u);  // round the bound up
+    if ((threadIdx.x & 31) == 0) atomicMax(out + 2 * blockIdx.y + which, __float_as_uint(m) + 1u);  // round up
 }
 
 // Spins until `n` consecutive tagged entries starting at p carry `tag`; lane t
@@ -405,20 +410,6 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                                 g = r1 ? d : g;
                                 v = r1 ? -inf : v;
                                 h = r1 ? d : h;
-                            }
-                            if (false) {
-                                const bool j1 = col == 0, r1 = row[q] == 1;
-                                g = (j1 || r1) ? d : g;
-                                v = r1 ? -inf : (j1 ? d : v);
-                                h = j1 ? -inf : (r1 ? d : h);
-                                if (a.bw != 0 && !in_band(row[q], col + 1, a.bw)) {
-                                    g = inf; v = inf; h = inf;
-                                }
-                            }
-                            if (false) {
-                                const int i = row[q], j = col + 1;
-                                if (i == a.N && j > a.N) lacc += (double)h;
-                                if (j == a.M && i > a.M) lacc += (double)v;
                             }
                             gdiag[q] = (active && k == kdiag[q]) ? g : gdiag[q];
                             vck[q] = (kl == ((t - 1) & 31)) ? v : vck[q];

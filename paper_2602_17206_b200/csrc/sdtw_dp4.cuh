@@ -158,7 +158,6 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
         __syncthreads();
         tc::tc_fence_after();
         tmem = tmem_slot + 128u * wk;  // this worker's 128 columns
-        tc_m2 = -2.0f * split_scale(A.absmax).inv;
     }
     const uint32_t tmem_lanes = (uint32_t)(32 * wk) << 16;  // lane quarter of the helper
     // probability tile slots k = 0..2 at base + kSlot k: pd, pu, pl [jj][t]
@@ -171,7 +170,6 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
     const unsigned epoch = A.epoch;
     const int total = a.B * a.S;
     const int ngroups_row = a.KK / 32;
-    const FxScales fx = fx_scales(A.absmax, a.N, a.M);
     for (;;) {
         if (warp == 1) {
             const unsigned tk1 = warp_ticket(&a.tickets[1]);
@@ -190,6 +188,8 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
         named_bar(1 + wk, 64);
         if ((int)tk >= total) break;
         const int s = a.S - 1 - (int)tk / a.B, b = (int)tk % a.B;
+        const FxScales fx = fx_scales(A.absmax + 2 * b, a.N, a.M);
+        if constexpr (kTc) tc_m2 = -2.0f * split_scale(A.absmax + 2 * b).inv;
         const int i = 32 * s + t + 1;
         const bool row_ok = i <= a.N;
         bool x_loaded = false;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                 // operand staging inside the target group's own slots (free)
                 uint8_t *stage = reinterpret_cast<uint8_t *>(base + kSlot * kWin * grp);
                 const uint32_t idesc = tc::idesc_f16_f32(128, 32);
-                const SplitScale sc = split_scale(A.absmax);
+                const SplitScale sc = split_scale(A.absmax + 2 * b_);
                 // raw fp32 staging after the three fp16 operand tiles (the
                 // probability slots, E tile and ring are all free until the
                 // recompute loop / epilogue)

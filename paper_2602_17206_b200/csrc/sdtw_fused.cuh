@@ -499,7 +499,6 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
         const bool leader = q == 0;
         uint8_t *xs = smem_raw + (size_t)p * ftc_slot_bytes(dpad);
         uint8_t *ys = xs + (size_t)128 * dpad * 4;
-        const SplitScale sc = split_scale(A.absmax);
         const uint32_t idesc = tc::idesc_f16_f32(128, 32);
         const int ksteps = dpad / 16, kbn = dpad / 8;
         unsigned u = 0;  // cumulative chunk count of this slot
@@ -521,6 +520,7 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
             const int ss = tk / a.B, b = tk % a.B;
             const float *xb = a.x + (size_t)b * a.N * a.D;
             const float *yb = a.y + (size_t)b * a.M * a.D;
+            const SplitScale sc = split_scale(A.absmax + 2 * b);
             // X: rows [128 ss + 64 q, +64) of the super-strip (previous MMAs done)
             for (int m = 0; m < 4; ++m) {
                 half_chunk_load(pre, xb, a.D, 128 * ss + 64 * q + 16 * m, a.N, a.D, kbn, t);
@@ -562,8 +562,6 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
                                                 (size_t)160 * dpad * 4) +
                       w * 2048;
         float *halo_s = sh.halo[warp];
-        const SplitScale sc = split_scale(A.absmax);
-        const float m2 = -2.0f * sc.inv;
         const float inf = Num<float>::inf();
         const uint32_t tq = tmem + 256u * p + ((uint32_t)(32 * w) << 16);
         unsigned u = 0;
@@ -575,6 +573,7 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
             if (tk >= total) break;
             const int ss = tk / a.B, b = tk % a.B;
             const int s = 4 * ss + w;
+            const float m2 = -2.0f * split_scale(A.absmax + 2 * b).inv;
             const unsigned base = n * Mu;  // cumulative column base of this super-strip
             if (s >= a.S) {
                 // no strip here: keep the ring protocol going

@@ -308,13 +308,14 @@ __global__ void finalize_grads_fx_add_kernel(const T *__restrict__ v, const long
                                              T *__restrict__ grad)
 {
     if (stats[2] == 0) return;  // no tile overflowed the store: nothing to add
-    const FxScales fx = fx_scales(absmax, N, M);
-    const double sm = 1.0 / (which == 0 ? fx.rs : fx.cs);
-    const double sa = 1.0 / (which == 0 ? fx.gx : fx.gy);
     const size_t total = (size_t)rows * D;
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (size_t)gridDim.x * blockDim.x) {
         const size_t r = idx / D;
+        const int b = (int)(r / (which == 0 ? N : M));
+        const FxScales fx = fx_scales(absmax + 2 * b, N, M);
+        const double sm = 1.0 / (which == 0 ? fx.rs : fx.cs);
+        const double sa = 1.0 / (which == 0 ? fx.gx : fx.gy);
         const double marg = (double)marg_fx[r] * sm;
         const double acc = (double)acc_fx[idx] * sa;
         if (marg != 0.0 || acc != 0.0) grad[idx] = (T)((double)grad[idx] + 2.0 * ((double)v[idx] * marg - acc));

@@ -227,7 +227,11 @@ __device__ __forceinline__ void split_store8_regs(const float4 (&v)[2], float s,
 
 }  // namespace tc
 
-// Power-of-two operand scales: |x * sx| <= 2^14, and 1/(sx sy).
+// Power-of-two operand scales: |x * sx| <= 2^14, and 1/(sx sy).  absmax
+// points at ONE pair's [max|x|, max|y|] (absmax[2 b], absmax[2 b + 1]): the
+// split, and so every fp32 cost, depends only on that pair's own series, so
+// a pair's results do not change with its batch-mates (sdtw(batch)[b] ==
+// sdtw(batch[b:b+1]) bit for bit).
 struct SplitScale {
     float sx, sy, inv;
 };
@@ -246,16 +250,17 @@ __device__ __forceinline__ SplitScale split_scale(const unsigned *absmax)
 }
 
 // Norms in double, rounded once (the cost epilogue's largest terms), and the
-// operand-scale maximum max|v| in the same pass: one warp per row, a fixed
-// butterfly reduction (deterministic).
+// operand-scale maximum max|v| of each pair in the same pass: one warp per
+// row, a fixed butterfly reduction (deterministic); row r belongs to pair
+// r / rpp and its maximum goes to absmax[2 (r / rpp) + which].
 __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__restrict__ x, int rows, int D,
-                                                               float *__restrict__ out, unsigned *absmax)
+                                                               float *__restrict__ out, unsigned *absmax, int rpp,
+                                                               int which)
 {
-    __shared__ float wmax[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    float mx = 0.f;
-    // grid-stride over rows (one warp per row): one atomic per block at the end
+    // grid-stride over rows (one warp per row)
     for (int r = blockIdx.x * 8 + w; r < rows; r += gridDim.x * 8) {
+        float mx = 0.f;
         const float *e = x + (size_t)r * D;
         double s = 0.0;
         if ((D & 3) == 0) {
@@ -275,15 +280,11 @@ __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__re
             }
         }
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-        if (lane == 0) out[r] = (float)s;
-    }
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-    if (lane == 0) wmax[w] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float m = wmax[0];
-        for (int q = 1; q < 8; ++q) m = fmaxf(m, wmax[q]);
-        if (m > 0.f) atomicMax(absmax, __float_as_uint(m));
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        if (lane == 0) {
+            out[r] = (float)s;
+            if (mx > 0.f) atomicMax(absmax + 2 * (r / rpp) + which, __float_as_uint(mx));
+        }
     }
 }
 
@@ -320,8 +321,6 @@ __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, i
     const int nblk = (R + rstride - 1) / rstride;  // blocks start at k rstride + roff (roff <= 0)
     const int kbn = dpad / 8;
     const size_t total = (size_t)B * nblk * rpb * kbn;
-    const SplitScale sc = split_scale(absmax);
-    const float s = which == 0 ? sc.sx : sc.sy;
     const bool vec = (D & 7) == 0;
     for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < total; u += (size_t)gridDim.x * blockDim.x) {
         const int r = (int)(u % rpb);        // row within the block (fastest: coalesced stores)
@@ -331,6 +330,8 @@ __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, i
         const int blk = (int)(bb % nblk);
         const int b = (int)(bb / nblk);
         const int row = blk * rstride + roff + r;
+        const SplitScale sc = split_scale(absmax + 2 * b);
+        const float s = which == 0 ? sc.sx : sc.sy;
         uint8_t *hi = dst + bb * (size_t)rpb * dpad * 4;
         uint8_t *lo = hi + (size_t)rpb * dpad * 2;
         const int k = kb * 8;
@@ -392,7 +393,6 @@ __global__ void __launch_bounds__(kCgThreads, 1)
     const int NB = (N + 127) / 128, JB = (M + 127) / 128;
     const int ntiles = B * NB * JB;
     const int rounds = dpad / kCgKR;
-    const SplitScale sc = split_scale(absmax);
     if (tid == 0) {
         for (int k = 0; k < kCgStages; ++k) {
             tc::mbar_init(&sh.st_full[k], 1);
@@ -532,7 +532,6 @@ __global__ void __launch_bounds__(kCgThreads, 1)
         const bool leader = hf == 0 && lane == 0;  // issues the quarter's bulk store
         // the cost stream must not push the operands (re-read per tile row) out of L2
         const uint64_t st_policy = tc::l2_evict_first_policy();
-        const float m2 = -2.0f * sc.inv;
         const int zb = (5 * hf) / G, ze = (5 * (hf + 1)) / G;  // this warp's 32-column chunks
         int li = 0;
         for (int n = t0; n < t1; ++n, ++li) {
@@ -540,6 +539,7 @@ __global__ void __launch_bounds__(kCgThreads, 1)
             tile_of(n, b, ib, jb);
             const int i0 = 128 * ib, j0 = 128 * jb;
             const int ab = li & 1;
+            const float m2 = -2.0f * split_scale(absmax + 2 * b).inv;
             const int i = i0 + 32 * q + lane;
             const bool row_ok = i < N;
             const float xi = row_ok ? xn[(size_t)b * N + i] : 0.f;
