@@ -15,16 +15,19 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsdtw_b200.so")
-SOURCES = ["sdtw_capi.cu"]
-HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
+# the host side (sdtw_capi.cu) and the DP kernels in their own translation
+# units (sdtw_kernels.h), compiled in parallel and linked into one library
+SOURCES = ["sdtw_capi.cu", "k_fwd_f32.cu", "k_fwd_f64.cu", "k_bwd4.cu", "k_bwd5_f32.cu", "k_bwd5_f64.cu",
+           "k_gemm.cu"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
+OBJDIR = os.path.join(HERE, "_obj")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
-    "--split-compile=0",
 ]
 
 
@@ -35,31 +38,52 @@ def _nvcc() -> str:
     return "nvcc"
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _obj(src: str) -> str:
+    return os.path.join(OBJDIR, src.replace(".cu", ".o"))
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps.append(os.path.join(ROOT, "include", "sdtw_capi.h"))
+    t = os.path.getmtime(target)
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp"]
-    cmd += [os.path.join(CSRC, f) for f in SOURCES]
-    cmd += ["-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "build.log")
-    with open(log, "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stderr[-8000:])
-        raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(LIB + ".tmp", LIB)
+    hdrs = [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "sdtw_capi.h")]
+    os.makedirs(OBJDIR, exist_ok=True)
+    todo = [src for src in SOURCES
+            if force or _stale(_obj(src), [os.path.join(CSRC, src)] + hdrs)]
+    procs = []
+    for src in todo:
+        cmd = [_nvcc(), *NVCC_FLAGS, "-c", "-o", _obj(src) + ".tmp", os.path.join(CSRC, src)]
+        procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log_parts, failed = [], []
+    for src, cmd, pr in procs:
+        out, err = pr.communicate()
+        log_parts.append(" ".join(cmd) + "\n" + out + err)
+        if pr.returncode != 0:
+            failed.append((src, err))
+        else:
+            os.replace(_obj(src) + ".tmp", _obj(src))
+    objs = [_obj(src) for src in SOURCES]
+    if not failed and (todo or _stale(LIB, objs)):
+        cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs, "-ldl"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        log_parts.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        if res.returncode != 0:
+            failed.append(("link", res.stderr))
+        else:
+            os.replace(LIB + ".tmp", LIB)
+    if todo:
+        with open(os.path.join(HERE, "build.log"), "w") as fh:
+            fh.write("\n".join(log_parts))
+    if failed:
+        for src, err in failed:
+            sys.stderr.write(f"--- {src}\n{err[-6000:]}\n")
+        raise RuntimeError(f"nvcc failed: {[f for f, _ in failed]} (see build.log)")
     if verbose:
-        sys.stdout.write(res.stderr)
+        sys.stdout.write("\n".join(log_parts))
     return LIB
 
 

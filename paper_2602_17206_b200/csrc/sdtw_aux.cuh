@@ -142,22 +142,24 @@ __device__ __forceinline__ T ref_lse3(T a, T b, T c)
     return m + log(exp(a - m) + exp(b - m) + exp(c - m));
 }
 
-// R table (double accumulation) from the row-major cost tensor.  Output in T.
-// forward.hpp:25-37 with R kept in double so the returned table is accurate
-// to the last bit of T.
+// R table from the row-major cost tensor, accumulated in T exactly as the
+// reference's forward<T> does (forward.hpp:25-37: R(i,j) = d + softmin(...)
+// in T), so an fp32 table carries the reference's own fp32 rounding drift --
+// the arithmetic the stability witness exercises (test_backward.cpp:286-321:
+// backward_linear<float> on that table overflows).  The engine's fast path
+// (sdtw_with_gradients) never forms R; this is the standalone-table API.
 template <class T>
 __global__ void __launch_bounds__(1024) table_forward_kernel(const T *__restrict__ d, int N, int M,
-                                                             int bw, double gamma,
-                                                             double *__restrict__ Rw,
+                                                             int bw, T gamma,
                                                              T *__restrict__ R_out)
 {
     const int b = blockIdx.x;
     const size_t W = (size_t)M + 2, cells = (size_t)(N + 2) * W;
-    double *R = Rw + (size_t)b * cells;
-    const double inf = Num<double>::inf();
+    T *R = R_out + (size_t)b * cells;
+    const T inf = Num<T>::inf();
     for (size_t c = threadIdx.x; c < cells; c += blockDim.x) R[c] = inf;
     __syncthreads();
-    if (threadIdx.x == 0) R[0] = 0.0;
+    if (threadIdx.x == 0) R[0] = T(0);
     __syncthreads();
     const T *db = d + (size_t)b * N * M;
     for (int p = 0; p <= N + M - 2; ++p) {
@@ -166,14 +168,11 @@ __global__ void __launch_bounds__(1024) table_forward_kernel(const T *__restrict
             const int cj = p - ci;
             if (!in_band(ci + 1, cj + 1, bw)) continue;
             const int i = ci + 1, j = cj + 1;
-            const double sm = ref_softmin<double>(R[(i - 1) * W + j - 1], R[(i - 1) * W + j],
-                                                  R[i * W + j - 1], gamma);
-            R[i * W + j] = (double)db[(size_t)ci * M + cj] + sm;
+            const T sm = ref_softmin<T>(R[(i - 1) * W + j - 1], R[(i - 1) * W + j], R[i * W + j - 1], gamma);
+            R[i * W + j] = db[(size_t)ci * M + cj] + sm;
         }
         __syncthreads();
     }
-    T *Ro = R_out + (size_t)b * cells;
-    for (size_t c = threadIdx.x; c < cells; c += blockDim.x) Ro[c] = (T)R[c];
 }
 
 // backward_sweep<T, Cost, kLog> (backward.hpp:29-177) on a given R table.

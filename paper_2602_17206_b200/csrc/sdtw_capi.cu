@@ -19,6 +19,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -29,6 +30,8 @@
 #include "sdtw_dp2.cuh"
 #include "sdtw_dp3.cuh"
 #include "sdtw_dp4.cuh"
+#include "sdtw_bwd5.cuh"
+#include "sdtw_kernels.h"
 #include "sdtw_fused.cuh"
 #include "sdtw_grad.cuh"
 #include "sdtw_tc.cuh"
@@ -190,6 +193,7 @@ struct sdtw_ctx {
     unsigned long long halo_sig[5] = {};
     unsigned epoch = 0;
     unsigned long long *trace = nullptr;  // debug: per-strip forward timestamps
+    unsigned dbg_counters[16] = {};       // debug: the last backward's counters
     cudaEvent_t ev[SDTW_NUM_PHASES][2] = {};
     bool ev_used[SDTW_NUM_PHASES] = {};
     // Host-pointer calls split the batch into pair chunks, each on its own
@@ -290,6 +294,22 @@ struct Out {
     }
 };
 
+// Launch of a kernel compiled in another translation unit (sdtw_kernels.h):
+// the arguments are converted to the kernel's parameter types first.
+template <class... P, class... A>
+void launch_ptr(sdtw_ctx *ctx, void (*fn)(P...), dim3 grid, dim3 block, size_t smem, A &&...a)
+{
+    static_assert(sizeof...(P) == sizeof...(A), "kernel argument count");
+    std::tuple<P...> args(static_cast<P>(std::forward<A>(a))...);
+    void *argv[sizeof...(P) > 0 ? sizeof...(P) : 1];
+    std::apply([&](auto &...v) {
+        size_t i = 0;
+        ((argv[i++] = (void *)&v), ...);
+    }, args);
+    CUDA_OK(cudaLaunchKernel((const void *)fn, grid, block, argv, smem, ctx->stream));
+    ++ctx->launches;
+}
+
 #define LAUNCH(ctx, kernel, grid, block, smem, ...)                         \
     do {                                                                    \
         kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);    \
@@ -352,6 +372,10 @@ void check_wait_timeouts()
     if (n != 0) {
         const int zero = 0;
         cudaMemcpyToSymbol(sdtw::g_sdtw_wait_timeouts, &zero, sizeof(int));
+    }
+    n += sdtw::take_timeouts_fwd_f32() + sdtw::take_timeouts_fwd_f64() + sdtw::take_timeouts_bwd4() +
+         sdtw::take_timeouts_bwd5_f32() + sdtw::take_timeouts_bwd5_f64();
+    if (n != 0) {
         fail(SDTW_ECUDA, "internal: " + std::to_string(n) + " wavefront dependency wait(s) timed out");
     }
 }
@@ -454,9 +478,9 @@ struct Pipeline {
         xn = Buf<T>(ctx, (size_t)B * N);
         yn = Buf<T>(ctx, (size_t)B * M);
         if constexpr (std::is_same<T, float>::value) {
-            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * N + 7) / 8), 256, 0, x,
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel<0>, (unsigned)std::min(ctx->sm_count * 8, (B * N + 7) / 8), 256, 0, x,
                    B * N, D, xn.p, absmax.p, N, 0);
-            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel, (unsigned)std::min(ctx->sm_count * 8, (B * M + 7) / 8), 256, 0, y,
+            LAUNCH(ctx, sdtw::norms_absmax_f32_kernel<0>, (unsigned)std::min(ctx->sm_count * 8, (B * M + 7) / 8), 256, 0, y,
                    B * M, D, yn.p, absmax.p, M, 1);
         } else {
             LAUNCH(ctx, sdtw::absmax_any_kernel<T>, dim3(grid_for((size_t)N * D, 256, 64), (unsigned)B), 256, 0, x,
@@ -475,7 +499,7 @@ struct Pipeline {
         const size_t total = (size_t)B * S * KK * 32;
         dsk = Buf<T>(ctx, total);
         if constexpr (std::is_same<T, float>::value) {
-            ensure_smem_attr(ctx->device, (const void *)sdtw::cost_gemm_tc_kernel, sdtw::kCgSmem);
+            ensure_smem_attr(ctx->device, (const void *)sdtw::k_cost_gemm(), sdtw::kCgSmem);
             // operands packed once (fp16 hi/lo core-matrix images), then
             // bulk-copied by every CTA that needs them
             const int NB = (N + 127) / 128;
@@ -483,12 +507,12 @@ struct Pipeline {
             // B operand of one N = 160 MMA per K step
             const int JB = (M + 127) / 128;
             Buf<uint8_t> xp(ctx, (size_t)B * NB * 128 * dpad * 4), yp(ctx, (size_t)B * JB * 160 * dpad * 4);
-            LAUNCH(ctx, sdtw::pack_split_kernel, grid_for(xp.n / 64, 256, 8192), 256, 0, x, B, N, D, dpad, 128,
+            LAUNCH(ctx, sdtw::pack_split_kernel<0>, grid_for(xp.n / 64, 256, 8192), 256, 0, x, B, N, D, dpad, 128,
                    absmax.p, 0, xp.p, 0, 0);
-            LAUNCH(ctx, sdtw::pack_split_kernel, grid_for(yp.n / 64, 256, 8192), 256, 0, y, B, M, D, dpad, 160,
+            LAUNCH(ctx, sdtw::pack_split_kernel<0>, grid_for(yp.n / 64, 256, 8192), 256, 0, y, B, M, D, dpad, 160,
                    absmax.p, 1, yp.p, 128, -32);
             const int ntiles = B * NB * ((M + 127) / 128);
-            LAUNCH(ctx, sdtw::cost_gemm_tc_kernel, (unsigned)std::min(ntiles, ctx->sm_count), sdtw::kCgThreads,
+            launch_ptr(ctx, sdtw::k_cost_gemm(), (unsigned)std::min(ntiles, ctx->sm_count), sdtw::kCgThreads,
                    sdtw::kCgSmem, xp.p, yp.p, xn.p, yn.p, absmax.p, B, N, M, S, C, KK, bw, dpad, dsk.p);
         } else {
             LAUNCH(ctx, sdtw::cost_skewed_kernel<T>, grid_for(total, 256), 256, 0, x, y, xn.p, yn.p, B,
@@ -575,22 +599,26 @@ struct Pipeline {
         A.tile_quota = tile_quota;
         A.stats = stats.p;
         A.trace = ctx->trace;
+        if (const char *e = std::getenv("SDTW_KNOBS"))  // experiments only
+            std::sscanf(e, "%d,%d,%d,%d", &A.knob[0], &A.knob[1], &A.knob[2], &A.knob[3]);
         return A;
     }
 
-    template <int K>
+    // one strip per warp: the lean step body (K == 1) beats strip ILP at
+    // every config measured (C5, 16384 strips: K=1 5.78 ms per Adam step,
+    // K=2 5.99, K=4 6.65)
     void launch_forward3()
     {
         auto A = args3();
         const int threads = 128;
         if (fused) {
-            auto kern = sdtw::sdtw_forward3_kernel<T, K, true>;
-            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, true>::kPerWarp * sizeof(T);
-            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, A);
+            auto kern = sdtw::k_forward3<T, 1, true>();
+            const size_t smem = 4 * sdtw::Fwd2Smem<T, 1, true>::kPerWarp * sizeof(T);
+            launch_ptr(ctx, kern, persistent_grid(kern, threads, smem, B * S), threads, smem, A);
         } else {
-            auto kern = sdtw::sdtw_forward3_kernel<T, K, false>;
-            const size_t smem = 4 * sdtw::Fwd2Smem<T, K, false>::kPerWarp * sizeof(T);
-            LAUNCH(ctx, kern, persistent_grid(kern, threads, smem, B * ((S + K - 1) / K)), threads, smem, A);
+            auto kern = sdtw::k_forward3<T, 1, false>();
+            const size_t smem = 4 * sdtw::Fwd2Smem<T, 1, false>::kPerWarp * sizeof(T);
+            launch_ptr(ctx, kern, persistent_grid(kern, threads, smem, B * S), threads, smem, A);
         }
     }
 
@@ -601,32 +629,24 @@ struct Pipeline {
         vc = Buf<T>(ctx, (size_t)B * C * N);
         lpart = Buf<double>(ctx, (size_t)B * S);
         flags = Buf<int>(ctx, 2 * (size_t)B * S + 2);
-        stats = Buf<unsigned>(ctx, 4);
+        stats = Buf<unsigned>(ctx, 16);
         CUDA_OK(cudaMemsetAsync(flags.p, 0, flags.n * sizeof(int), ctx->stream));
-        CUDA_OK(cudaMemsetAsync(stats.p, 0, 4 * sizeof(unsigned), ctx->stream));
+        CUDA_OK(cudaMemsetAsync(stats.p, 0, 16 * sizeof(unsigned), ctx->stream));
         Phase ph(ctx, 2);
-        // strips per warp: enough warps to fill the device first, ILP second
-        const int strips = B * S;
-        const int slots = ctx->sm_count * 16;
         if (tc_fused) {
             if constexpr (std::is_same<T, float>::value) {
                 auto A = args3();
                 const size_t smem = 2 * sdtw::ftc_slot_bytes(dpad);
-                ensure_smem_attr(ctx->device, (const void *)sdtw::sdtw_forward_tc_kernel,
+                ensure_smem_attr(ctx->device, (const void *)sdtw::k_forward_tc(),
                                  (int)(2 * sdtw::ftc_slot_bytes(sdtw::kFtcMaxD)));
                 const int work = B * ((S + 3) / 4);
                 const unsigned grid = (unsigned)std::max(1, std::min((work + 1) / 2, ctx->sm_count));
-                LAUNCH(ctx, sdtw::sdtw_forward_tc_kernel, grid, sdtw::kFtcThreads, smem, A, ftc());
+                launch_ptr(ctx, sdtw::k_forward_tc(), grid, sdtw::kFtcThreads, smem, A, ftc());
             }
-        } else if (!fused) {
-            // one strip per warp: the lean step body (K == 1) beats strip ILP
-            // at every config measured (C5, 16384 strips: K=1 5.78 ms per Adam
-            // step, K=2 5.99, K=4 6.65)
-            launch_forward3<1>();
-        } else if (strips >= 4 * slots) launch_forward3<4>();
-        else if (strips >= 2 * slots) launch_forward3<2>();
-        else launch_forward3<1>();
-        LAUNCH(ctx, sdtw::sdtw_loss_reduce_kernel, grid_for(B, 128), 128, 0, lpart.p, B, S, loss_f,
+        } else {
+            launch_forward3();
+        }
+        LAUNCH(ctx, sdtw::sdtw_loss_reduce_kernel<0>, grid_for(B, 128), 128, 0, lpart.p, B, S, loss_f,
                loss_d);
     }
 
@@ -675,31 +695,25 @@ struct Pipeline {
         {
             Phase ph(ctx, 3);
             if (tc_fused) {
-                auto kern = sdtw::sdtw_backward4_kernel<T, false, true>;
-                constexpr int kW = sdtw::bwd_workers<true>();
-                const size_t smem = kW * sdtw::Bwd4Smem<T, false, true>::kWorkerBytes;
-                // TMEM-using kernels run one CTA per SM (measured with the
-                // occupancy API), so the CTA carries kW workers (2 x 128 columns)
-                static_assert(kW * sdtw::Bwd4Smem<float, false, true>::kWorkerBytes <= 232448,
-                              "fused backward workers must fit one CTA");
-                LAUNCH(ctx, kern, persistent_grid(kern, 64 * kW, smem, 2 * B * S), 64 * kW, smem, A, stat, ftc());
-            } else if (fused) {
-                auto kern = sdtw::sdtw_backward4_kernel<T, true>;
-                const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, sdtw::FusedTcArgs{});
+                if constexpr (std::is_same<T, float>::value) {
+                    auto kern = sdtw::k_backward4<float, false, true, 3>();
+                    constexpr int kW = sdtw::bwd_workers<true>();
+                    const size_t smem = kW * sdtw::Bwd4Smem<T, false, true>::kWorkerBytes;
+                    // TMEM-using kernels run one CTA per SM (measured with the
+                    // occupancy API), so the CTA carries kW workers (2 x 128 columns)
+                    static_assert(kW * sdtw::Bwd4Smem<float, false, true>::kWorkerBytes <= 232448,
+                                  "fused backward workers must fit one CTA");
+                    launch_ptr(ctx, kern, persistent_grid(kern, 64 * kW, smem, 2 * B * S), 64 * kW, smem, A, stat,
+                               ftc());
+                }
             } else {
-                // recompute window: 3 tiles per request where alignment bands
-                // are narrow and strips few (C2: 0.447 vs 0.455 ms, C3: 1.63
-                // vs 1.72 ms), 2 (three workers per SM) where bands are wide
-                // or strips many (C1 backward -16 %, C5 -25 %)
-                const bool win2 = gamma >= 0.5 || (size_t)B * S > 8192;
-                auto kern = win2 ? sdtw::sdtw_backward4_kernel<T, false, false, 2>
-                                 : sdtw::sdtw_backward4_kernel<T, false, false, 3>;
-                const size_t smem = (win2 ? sdtw::Bwd4Smem<T, false, false, 2>::kPerWarp
-                                          : sdtw::Bwd4Smem<T, false, false, 3>::kPerWarp) *
-                                    sizeof(T);
-                LAUNCH(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat, sdtw::FusedTcArgs{});
+                launch_backward5(A);
             }
+        }
+        if (ctx->trace) {  // diagnostics: the backward's counters (sdtw_debug_counters)
+            CUDA_OK(cudaMemcpyAsync(ctx->dbg_counters, stats.p, sizeof ctx->dbg_counters, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+            CUDA_OK(cudaStreamSynchronize(ctx->stream));
         }
         if (gx || gy) {
             // ordered, atomic-free contraction of the stored tiles
@@ -720,11 +734,11 @@ struct Pipeline {
                 Buf<int> cnt(ctx, (size_t)nc), off(ctx, (size_t)nc + 1), ord(ctx, cap);
                 CUDA_OK(cudaMemsetAsync(cnt.p, 0, cnt.n * sizeof(int), ctx->stream));
                 const unsigned tg = grid_for(cap, 256, (unsigned)ctx->sm_count * 8);
-                LAUNCH(ctx, sdtw::tile_hist_kernel, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C, cnt.p);
-                LAUNCH(ctx, sdtw::exclusive_scan_kernel, 1, 1024, 0, cnt.p, nc, off.p);
-                LAUNCH(ctx, sdtw::tile_scatter_kernel, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C,
+                LAUNCH(ctx, sdtw::tile_hist_kernel<0>, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C, cnt.p);
+                LAUNCH(ctx, sdtw::exclusive_scan_kernel<0>, 1, 1024, 0, cnt.p, nc, off.p);
+                LAUNCH(ctx, sdtw::tile_scatter_kernel<0>, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C,
                        off.p, cnt.p, ord.p);
-                LAUNCH(ctx, sdtw::segment_sort_kernel, grid_for(nc, 128), 128, 0, off.p, ord.p, tile_meta.p, nc);
+                LAUNCH(ctx, sdtw::segment_sort_kernel<0>, grid_for(nc, 128), 128, 0, off.p, ord.p, tile_meta.p, nc);
                 LAUNCH(ctx, contract, std::min<unsigned>(nc * nkb, cg), 256, 0, tiles.p,
                        tile_meta.p, strip_tiles.p, tile_quota, off.p, ord.p, 1, B, S, C, N, M, D, y, x, gy);
             }
@@ -739,6 +753,28 @@ struct Pipeline {
         }
         // the cost tensor is dropped after the backward (backward.hpp:291)
         dsk = Buf<T>();
+    }
+
+    // The per-pair pipeline backward (sdtw_bwd5.cuh): one CTA per pair, E
+    // warps + recompute helpers, P tiles in a per-CTA pool.
+    Buf<T> pool, spill;
+    void launch_backward5(sdtw::Dp3Args<T> &A)
+    {
+        constexpr int NE = 4, NH = 12;
+        using Sh = sdtw::Bwd5Shared<T, NE, NH>;
+        const size_t smem = sizeof(Sh);
+        auto kern = fused ? sdtw::k_backward5<T, 1, NE, NH>() : sdtw::k_backward5<T, 0, NE, NH>();
+        ensure_smem_attr(ctx->device, (const void *)kern, (int)smem);
+        int occ = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * (NE + NH), smem));
+        if (occ < 1) fail(SDTW_ECUDA, "backward5 does not fit on an SM");
+        const int grid = std::max(1, std::min(B, occ * ctx->sm_count));
+        if (C > sdtw::kB5MaxC) fail(SDTW_EINVAL, "backward: M > 131072 columns is not supported");
+        pool = Buf<T>(ctx, (size_t)grid * sdtw::kB5NQ * C * 3 * 1024);
+        spill = Buf<T>(ctx, (size_t)grid * 2 * NE * M);
+        int *timeouts = nullptr;
+        CUDA_OK(cudaGetSymbolAddress((void **)&timeouts, sdtw::g_sdtw_wait_timeouts));
+        launch_ptr(ctx, kern, grid, 32 * (NE + NH), smem, A, pool.p, spill.p, timeouts);
     }
 
     void grads(T *gx, T *gy)
@@ -978,9 +1014,8 @@ int forward_api(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_
             LAUNCH(ctx, sdtw::cost_rowmajor_kernel<T>, grid_for(B * N * M, 256), 256, 0, xi.p, yi.p,
                    pl.xn.p, pl.yn.p, (int)B, (int)N, (int)M, (int)D, d);
             if (ro.p) {
-                Buf<double> rw(ctx, B * (N + 2) * (M + 2));
                 LAUNCH(ctx, sdtw::table_forward_kernel<T>, (unsigned)B, 1024, 0, d, (int)N, (int)M,
-                       (int)cfg->bandwidth, (double)(T)cfg->gamma, rw.p, ro.p);
+                       (int)cfg->bandwidth, (T)cfg->gamma, ro.p);
             }
         }
         lo.finish(ctx);
@@ -1300,6 +1335,18 @@ int sdtw_debug_set_trace(sdtw_ctx *ctx, void *trace_dev)
     if (!ctx) return SDTW_EINVAL;
     ctx->trace = static_cast<unsigned long long *>(trace_dev);
     return SDTW_OK;
+}
+
+int sdtw_debug_counters(sdtw_ctx *ctx, unsigned *out, int n)
+{
+    if (!ctx || !out) return SDTW_EINVAL;
+    for (int i = 0; i < n && i < 16; ++i) out[i] = ctx->dbg_counters[i];
+    return SDTW_OK;
+}
+
+int sdtw_debug_waits(int dtype64, int *out, int n)
+{
+    return dtype64 ? sdtw::take_b5_dbg_f64(out, n) : sdtw::take_b5_dbg_f32(out, n);
 }
 
 const char *sdtw_last_error(void) { return g_err.c_str(); }

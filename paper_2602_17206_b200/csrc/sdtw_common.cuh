@@ -107,7 +107,9 @@ __device__ __forceinline__ int flag_acquire(const int *p)
 }
 // Set when a dependency wait gave up (a scheduling bug, never expected); the
 // host turns it into an error instead of letting a kernel spin forever.
-__device__ int g_sdtw_wait_timeouts = 0;
+// One copy per translation unit (the kernels live in several); the host
+// reads and clears every copy after a call (check_wait_timeouts).
+static __device__ int g_sdtw_wait_timeouts = 0;
 
 // Every lane performs its own acquire so its later plain loads are ordered.
 // Bounded: after ~2^24 polls (tens of seconds) the wait is abandoned and

@@ -80,6 +80,7 @@ __device__ __forceinline__ unsigned warp_ticket(unsigned *counter)
 }
 
 // Sums strip partials in strip order (deterministic).
+template <int kTU = 0>
 __global__ void sdtw_loss_reduce_kernel(const double *lpart, int B, int S, float *lf,
                                         double *ld)
 {

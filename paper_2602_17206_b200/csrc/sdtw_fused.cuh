@@ -459,6 +459,7 @@ for (int e = 0; e < 5; ++e)
 // tickets and issues the MMAs).  Tickets over super-strips (strip-major,
 // pair-minor) from a.tickets[0].
 // ---------------------------------------------------------------------------
+template <int kTU = 0>
 __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args<float> A, FusedTcArgs F)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];

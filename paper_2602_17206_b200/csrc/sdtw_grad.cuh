@@ -20,6 +20,7 @@
 namespace sdtw {
 
 // Chunk buckets: count the stored tiles of each (b, c).
+template <int kTU = 0>
 __global__ void tile_hist_kernel(const int4 *__restrict__ meta, const int *__restrict__ strip_tiles, int quota,
                                  int nstrips, int C, int *cnt_c)
 {
@@ -32,6 +33,7 @@ __global__ void tile_hist_kernel(const int4 *__restrict__ meta, const int *__res
 }
 
 // Exclusive scan of cnt[0..n) into off[0..n] (one block).
+template <int kTU = 0>
 __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int *__restrict__ cnt, int n, int *__restrict__ off)
 {
     __shared__ int warp_sums[32];
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(1024) exclusive_scan_kernel(const int *__restr
 
 // Bucket fill: cnt is consumed (counted down), so positions are unique;
 // the order inside a bucket is fixed afterwards by segment_sort_kernel.
+template <int kTU = 0>
 __global__ void tile_scatter_kernel(const int4 *__restrict__ meta, const int *__restrict__ strip_tiles, int quota,
                                     int nstrips, int C, const int *__restrict__ off_c, int *cnt_c, int *ord_c)
 {
@@ -82,6 +85,7 @@ __global__ void tile_scatter_kernel(const int4 *__restrict__ meta, const int *__
 }
 
 // Insertion sort of each chunk bucket by strip (meta.y).
+template <int kTU = 0>
 __global__ void segment_sort_kernel(const int *__restrict__ off, int *ord, const int4 *__restrict__ meta, int nseg)
 {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nseg; k += gridDim.x * blockDim.x) {

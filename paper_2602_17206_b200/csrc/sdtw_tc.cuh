@@ -252,17 +252,28 @@ __device__ __forceinline__ SplitScale split_scale(const unsigned *absmax)
 // Norms in double, rounded once (the cost epilogue's largest terms), and the
 // operand-scale maximum max|v| of each pair in the same pass: one warp per
 // row, a fixed butterfly reduction (deterministic); row r belongs to pair
-// r / rpp and its maximum goes to absmax[2 (r / rpp) + which].
+// r / rpp and its maximum goes to absmax[2 (r / rpp) + which].  Each CTA
+// owns a contiguous row range, so a warp's rows mostly share one pair and it
+// flushes its running maximum with one atomic per pair it touched.
+template <int kTU = 0>
 __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__restrict__ x, int rows, int D,
                                                                float *__restrict__ out, unsigned *absmax, int rpp,
                                                                int which)
 {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // grid-stride over rows (one warp per row)
-    for (int r = blockIdx.x * 8 + w; r < rows; r += gridDim.x * 8) {
-        float mx = 0.f;
+    const int per = (rows + gridDim.x - 1) / gridDim.x;
+    const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+    float mx = 0.f;
+    int pair = -1;
+    for (int r = r0 + w; r < r1; r += 8) {
+        if (r / rpp != pair) {
+            if (pair >= 0 && lane == 0 && mx > 0.f) atomicMax(absmax + 2 * pair + which, __float_as_uint(mx));
+            pair = r / rpp;
+            mx = 0.f;
+        }
         const float *e = x + (size_t)r * D;
         double s = 0.0;
+        float m = 0.f;
         if ((D & 3) == 0) {
             for (int k = 4 * lane; k < D; k += 128) {
                 const float4 v = __ldg(reinterpret_cast<const float4 *>(e + k));
@@ -270,22 +281,21 @@ __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__re
                 s = fma((double)v.y, (double)v.y, s);
                 s = fma((double)v.z, (double)v.z, s);
                 s = fma((double)v.w, (double)v.w, s);
-                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+                m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
             }
         } else {
             for (int k = lane; k < D; k += 32) {
                 const float v = e[k];
                 s = fma((double)v, (double)v, s);
-                mx = fmaxf(mx, fabsf(v));
+                m = fmaxf(m, fabsf(v));
             }
         }
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
-        if (lane == 0) {
-            out[r] = (float)s;
-            if (mx > 0.f) atomicMax(absmax + 2 * (r / rpp) + which, __float_as_uint(mx));
-        }
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+        mx = fmaxf(mx, m);
+        if (lane == 0) out[r] = (float)s;
     }
+    if (pair >= 0 && lane == 0 && mx > 0.f) atomicMax(absmax + 2 * pair + which, __float_as_uint(mx));
 }
 
 __device__ __forceinline__ void named_bar_cg(int id, int threads)
@@ -313,6 +323,7 @@ __device__ __forceinline__ float tc_cost(float acc, float xi, float yj, float m2
 // ----------------------------------------------------------------------------
 // Block k covers rows [k rstride + roff, + rpb) (rstride = rpb, roff = 0 for
 // a plain tiling; the GEMM's B operand uses overlapping 160-row blocks).
+template <int kTU = 0>
 __global__ void pack_split_kernel(const float *__restrict__ src, int B, int R, int D, int dpad, int rpb,
                                   const unsigned *absmax, int which, uint8_t *__restrict__ dst, int rstride = 0,
                                   int roff = 0)
@@ -382,6 +393,7 @@ struct CgShared {
 // walks tiles (b, ib, jb) with the producer warp loading round g + 1 while
 // the MMAs of round g run, and the epilogue warps draining tile n - 1
 // from the other TMEM accumulator (2 x 160 columns) while tile n is computed.
+template <int kTU = 0>
 __global__ void __launch_bounds__(kCgThreads, 1)
     cost_gemm_tc_kernel(const uint8_t *__restrict__ xp, const uint8_t *__restrict__ yp, const float *__restrict__ xn,
                         const float *__restrict__ yn, const unsigned *absmax, int B, int N, int M, int S, int C,
