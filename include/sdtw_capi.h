@@ -102,6 +102,9 @@ int sdtw_debug_counters(sdtw_ctx *ctx, unsigned *out, int n);
 /* Diagnostics: the backward's timed-out dependency waits since the last
  * call, out[0] = count, then (site, CTA, a, b) records; returns the count. */
 int sdtw_debug_waits(int dtype64, int *out, int n);
+/* Diagnostics (timing enabled): per phase 0 = not started, 1 = started,
+ * 3 = finished (non-blocking event queries; -1 = phase did not run). */
+int sdtw_debug_phase_status(sdtw_ctx *ctx, int *out, int n);
 
 const char *sdtw_last_error(void);
 size_t sdtw_last_oom_bytes(void);

@@ -50,6 +50,11 @@ def _stale(target: str, deps) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    global LIB, OBJDIR, NVCC_FLAGS
+    if os.environ.get("SDTW_BUILD_DEBUG"):  # bounds-checked variant (experiments)
+        LIB = os.path.join(HERE, "libsdtw_dbg.so")
+        OBJDIR = os.path.join(HERE, "_obj_dbg")
+        NVCC_FLAGS = NVCC_FLAGS + ["-DSDTW_B5_DEBUG"]
     hdrs = [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "sdtw_capi.h")]
     os.makedirs(OBJDIR, exist_ok=True)
     todo = [src for src in SOURCES

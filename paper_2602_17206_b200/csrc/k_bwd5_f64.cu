@@ -23,6 +23,8 @@ int take_b5_dbg_f64(int *out, int n)
     return h[0];
 }
 
+void set_b5_spin_limit_f64(unsigned v) { cudaMemcpyToSymbol(g_b5_spin_limit, &v, sizeof v); }
+
 SDTW_TU_TIMEOUTS(bwd5_f64)
 
 }  // namespace sdtw

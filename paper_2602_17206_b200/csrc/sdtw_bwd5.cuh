@@ -34,6 +34,7 @@
 // by the recompute one row per step as well).
 #pragma once
 #include <climits>
+#include <cstdio>
 #include <type_traits>
 #include "sdtw_common.cuh"
 #include "sdtw_dp.cuh"
@@ -57,7 +58,8 @@ struct Bwd5Shared {
     T et[NE][3][32][33];       // E tile staging, rotated rows (three tiles in flight)
     T hhalo[NH][kB5Win][32];   // helper: top halos of the window's tiles
     int ring_strip[NE][2];     // strip the ring serves
-    int zero_above[NE][2];     // columns >= zero_above: S = 0
+    int zero_above[NE][2];     // columns >= zero_above: S = 0 (-1 until the producer knows: its
+                               // first sweep starts there, or it is dead: 0)
     int prod_pos[NE][2];       // columns >= prod_pos: decided (ring or zero)
     int intent_pos[NE][2];     // lowest column the producer is writing or has written
     int zero_below[NE][2];     // columns < zero_below: S = 0 (decided)
@@ -72,8 +74,24 @@ struct Bwd5Shared {
     int job_seq[2][kB5JQ], job_rd[2][kB5JQ];
     int job_tail[2], job_head[2];
     int done;                           // the pair's strips are finished: helpers leave
+    int4 hjob[NH];                      // a helper's current job (lane 0 -> warp)
     int pair;
 };
+
+#ifdef SDTW_B5_DEBUG
+#define B5_CHECK(cond, tag, a, b)                                                                     \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("B5_CHECK %s failed: blk %d warp %d lane %d a=%lld b=%lld\n", tag, blockIdx.x,      \
+                   threadIdx.x >> 5, threadIdx.x & 31, (long long)(a), (long long)(b));               \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define B5_CHECK(cond, tag, a, b) \
+    do {                          \
+    } while (0)
+#endif
 
 __device__ __forceinline__ int vld(const int &p) { return *(const volatile int *)&p; }
 __device__ __forceinline__ unsigned vldu(const unsigned &p) { return *(const volatile unsigned *)&p; }
@@ -84,6 +102,7 @@ __device__ __forceinline__ unsigned b5_tag(int s, int c) { return ((unsigned)s <
 // Bounded spin (a scheduling bug must surface as an error, not a hang).
 // (trace mode: a timed-out wait also records (site, CTA, a, b) in g_b5_dbg)
 static __device__ int g_b5_dbg[4 + 4 * 64];
+static __device__ unsigned g_b5_spin_limit = 1u << 24;  // experiments: set through knob[2]
 struct B5Spin {
     unsigned n = 0;
     int *timeouts;
@@ -93,7 +112,7 @@ struct B5Spin {
     }
     __device__ __forceinline__ bool go(int lane)
     {
-        if (++n > (1u << 26)) {
+        if (++n > g_b5_spin_limit) {
             if (lane == 0) {
                 atomicAdd(timeouts, 1);
                 const int k = atomicAdd(&g_b5_dbg[0], 1);
@@ -154,6 +173,8 @@ __device__ void b5_enqueue(Bwd5Shared<T, NE, NH> &sh, int qu, int4 job, int *tim
     B5Spin sq(timeouts, 3, job.x, slot);
     while (vld(sh.job_rd[qu][p]) != slot - cap)  // previous occupant taken by a helper
         if (!sq.go(0)) break;
+    B5_CHECK(job.z >= 1 && job.z <= kB5Win, "enqueue", (long long)slot * 1000 + qu * 100 + p,
+             (long long)job.x * 1000000 + job.y * 1000 + job.z);
     sh.jobs[qu][p] = job;
     __threadfence_block();
     vst(sh.job_seq[qu][p], slot + 1);
@@ -296,6 +317,7 @@ __device__ void b5_recompute(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *
                         prob_cell<T>(d, u[z], lc[z], a.k, a.gln2, v, hh, pd, pu, pl);
                     }
                     if (act) {
+                        B5_CHECK(cr - z >= 0 && cr - z < a.C && s >= 0 && s < a.S, "recompute tile", s, cr - z);
                         T *p = dst[z] + (qq & 31) * 32;
                         p[0] = pd;
                         p[1024] = pu;
@@ -331,10 +353,17 @@ __device__ void b5_helper(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *myp
                         const int cap = qu ? kB5UQ : kB5JQ;
                         const int p = hd % cap;
                         B5Spin sw(timeouts, 10, hd, qu);
+                        bool ok = true;
                         while (vld(sh.job_seq[qu][p]) != hd + 1)
-                            if (!sw.go(0)) break;
+                            if (!sw.go(0)) {
+                                ok = false;
+                                break;
+                            }
                         __threadfence_block();
                         job = sh.jobs[qu][p];
+                        B5_CHECK(job.z >= 1, "job read", (long long)hd * 1000 + qu * 100 + p,
+                                 (long long)job.x * 1000000 + job.y * 1000 + job.z);
+                        if (!ok) job = make_int4(-1, 0, 0, 0);  // never run a half-published job
                         __threadfence_block();
                         vst(sh.job_rd[qu][p], hd);
                         got = true;
@@ -346,13 +375,22 @@ __device__ void b5_helper(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *myp
                 if (!sp.go(0)) break;
             }
         }
-        job.x = __shfl_sync(kFull, job.x, 0);
-        job.y = __shfl_sync(kFull, job.y, 0);
-        job.z = __shfl_sync(kFull, job.z, 0);
+        // broadcast through shared memory behind a warp barrier (lane 0 may
+        // have spun in its own loop above)
+        if (t == 0) sh.hjob[h] = job;
+        __syncwarp();
+        job = sh.hjob[h];
+        __syncwarp();
         if (job.x < 0) return;
+        B5_CHECK(job.x < A.a.S && job.y >= 0 && job.y < A.a.C && job.z >= 1 && job.z <= kB5Win && job.y - job.z + 1 >= 0,
+                 "job", job.x * 65536 + job.y, job.z);
         const int q = job.x % kB5NQ;
-        // skip a window its strip's E warp is already past (wasted work)
-        const bool live = vld(sh.e_pos[q]) >= job.y - job.z + 1;
+        // skip a window its strip's E warp is already past (wasted work);
+        // decided by lane 0 (e_pos moves under us: every lane must agree,
+        // the recompute is full of warp collectives)
+        bool live = false;
+        if (t == 0) live = vld(sh.e_pos[q]) >= job.y - job.z + 1;
+        live = __shfl_sync(kFull, live, 0);
         const long long tw1 = tr ? clock64() : 0;
         if (live) b5_recompute<T, kCost, NE, NH>(sh, A, mypool, b, job.x, job.y, job.z, h, t);
         if (tr && t == 0) {
@@ -360,7 +398,9 @@ __device__ void b5_helper(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *myp
             b5_count(A.trace, A.stats, 13, (clock64() - tw1) >> 10);
             b5_count(A.trace, A.stats, 14, (tw1 - tw0) >> 10);
         }
-        __threadfence_block();
+        // the E warp reads the pool through L2 (ld.global.cg): the tiles must
+        // be visible there before the ready bits are
+        __threadfence();
         __syncwarp();
         if (t == 0) {
             for (int z = 0; z < job.z; ++z) {
@@ -417,26 +457,38 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
     if (!bottom) {
         if (t == 0) {
             B5Spin sp(timeouts, 6, s, vld(sh.ring_strip[kb][rb]));
-            while (vld(sh.ring_strip[kb][rb]) != s + 1)
+            while (vld(sh.ring_strip[kb][rb]) != s + 1 || vld(sh.zero_above[kb][rb]) < 0)
                 if (!sp.go(0)) break;
             __threadfence_block();
             zab = vld(sh.zero_above[kb][rb]);
         }
+        __syncwarp();  // lane 0 spun alone above: reconverge before the broadcast
         zab = __shfl_sync(kFull, zab, 0);
         c0 = zab > 0 ? (zab - 1) >> 5 : -1;
     }
     if (tr && t == 0) b5_count(A.trace, A.stats, 15, (clock64() - cy_start) >> 10);
-    // ---- 3. publish my ring
-    const int za = c0 >= 0 ? min(M, 32 * (c0 + 1)) : 0;
+    // ---- 3. publish my ring; its upper bound (zero_above) follows when this
+    // strip's first sweep starts (everything right of it is dead for the
+    // strip above, which then starts right there instead of scanning)
     if (t == 0) {
-        vst(sh.zero_above[k][rme], za);
-        vst(sh.prod_pos[k][rme], za);
-        vst(sh.intent_pos[k][rme], za);
+        vst(sh.zero_above[k][rme], -1);
+        vst(sh.prod_pos[k][rme], M);
+        vst(sh.intent_pos[k][rme], M);
         vst(sh.zero_below[k][rme], 0);
-        vst(sh.cons_pos[k][rme], top ? INT_MIN : za);
+        vst(sh.cons_pos[k][rme], top ? INT_MIN : M);
         __threadfence_block();
         vst(sh.ring_strip[k][rme], s);
     }
+    bool za_known = false;
+    auto publish_top = [&](int za) {  // no S >= za from this strip
+        if (!za_known && t == 0) {
+            vst(sh.prod_pos[k][rme], za);
+            vst(sh.intent_pos[k][rme], za);
+            __threadfence_block();
+            vst(sh.zero_above[k][rme], za);
+        }
+        za_known = true;
+    };
     // S from below for columns [jl, jh] decided?  (bottom strip: all zero)
     auto wait_below = [&](int jl, int jh) -> int {
         int zb = 0;
@@ -452,16 +504,37 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
             __threadfence_block();
         }
         if (tr) cy_below += clock64() - c0_;
+        __syncwarp();  // lane 0 spun alone above: reconverge before the broadcast
         return __shfl_sync(kFull, zb, 0);
     };
-    // (valid once the producer decided column j: wait_below)
+    // (valid once the producer decided column j: wait_below).  Read the
+    // ring first, then check that the producer had not started writing
+    // column j - kB5Ring (which overwrites the slot): else the global copy.
     auto s_below = [&](int j, int zb) -> T {
         if (bottom || j >= zab || j < zb) return T(0);
+        B5_CHECK(j >= 0 && j < M, "s_below", j, zb);
         const T v = ring_b[j & (kB5Ring - 1)];
         __threadfence_block();
-        // overwritten (or being overwritten) by column j - kB5Ring: global copy
         if (vld(sh.intent_pos[kb][rb]) > j - kB5Ring) return v;
         return ldcg(spill_b + j);
+    };
+    // the 8 columns hi, hi-1, .., hi-7 (>= lo) at once: one validation
+    auto s_below8 = [&](int hi, int lo, int zb, T (&o)[8]) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int j = hi - kk;
+            o[kk] = (bottom || j < lo || j >= zab || j < zb) ? T(0) : ring_b[j & (kB5Ring - 1)];
+        }
+        if (bottom) return;
+        __threadfence_block();
+        const int ip = vld(sh.intent_pos[kb][rb]);
+        if (ip <= hi - kB5Ring) {  // rare: fell behind the ring
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int j = hi - kk;
+                if (j >= lo && j < zab && j >= zb && ip <= j - kB5Ring) o[kk] = ldcg(spill_b + j);
+            }
+        }
     };
 
     T e_right = T(0), pl_right = T(0), pd_right = T(0), s_prev = T(0);
@@ -521,6 +594,7 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
                 if (ir <= a.N && t < width) a.E[((size_t)b * a.N + (ir - 1)) * a.M + j0 + t] = v[r];
             }
         }
+        B5_CHECK(cc >= 0 && cc < a.C && nstored <= a.C, "flush", cc, nstored);
         if (nstored < A.tile_quota) {
             const size_t slot = ((size_t)b * a.S + s) * A.tile_quota + nstored;
             T *dt = A.tiles + slot * 1024;
@@ -558,8 +632,9 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
             if (zb > jh) break;  // everything from here left is dead
             const T sv = (jl + t <= jh) ? s_below(jl + t, zb) : T(0);
             if (__any_sync(kFull, sv != T(0))) goto sweep;
-            // dead chunk: zero S for the strip above
-            if (!top) {
+            // dead chunk: zero S for the strip above (nothing to write while
+            // no sweep has started: it is above this strip's zero_above)
+            if (!top && za_known) {
                 if (t == 0) vst(sh.intent_pos[k][rme], jl);
                 __syncwarp();
                 __threadfence_block();
@@ -578,6 +653,7 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
         }
     sweep:
         // ---------------- sweep from chunk c ----------------
+        publish_top(min(M, 32 * c + 32));
         const int J = 32 * c + 31;
         int Jstop = INT_MIN;  // columns < Jstop are outside the run (set when it ends)
         int lowest = c;       // lowest chunk lane 31 entered
@@ -587,6 +663,31 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
         tile_ready(c);
         if (t == 0) vst(sh.e_pos[q], c);
         bool nz_tile = false;  // any E != 0 in the newest tile so far
+        // probabilities of a sub-group's cells (rotated rows r, uniform),
+        // loaded from the pool one sub-group ahead; only tiles >= lowest are
+        // known ready, so an entry sub-group reloads its new tile's cells
+        T pd8[8], pu8[8], pl8[8], pdn[8], pun[8], pln[8];
+        auto load_p = [&](int l31x, int lowx, T (&pd)[8], T (&pu)[8], T (&pl)[8], bool only_new, int newc) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int j = l31x - kk + 31 - t;
+                bool ld = j >= Jstop && j <= J && j >= 32 * lowx && j >= 0;
+                if (only_new) ld = ld && (j >> 5) == newc;
+                if (ld) {
+                    const int cj = j >> 5;
+                    B5_CHECK(cj >= 0 && cj < a.C, "P load", cj, j);
+                    const T *pt = mypool + ((size_t)q * a.C + cj) * 3 * 1024 + ((l31x - kk + 31) & 31) * 32 + t;
+                    pd[kk] = ldcg(pt);
+                    pu[kk] = ldcg(pt + 1024);
+                    pl[kk] = ldcg(pt + 2048);
+                } else if (!only_new) {
+                    pd[kk] = T(0);
+                    pu[kk] = T(0);
+                    pl[kk] = T(0);
+                }
+            }
+        };
+        load_p(J, lowest, pdn, pun, pln, false, 0);
         for (int g = 0;; ++g) {
             const int k0 = 8 * g;
             const int l31 = J - k0;  // lane 31's column at the sub-group's first step
@@ -604,6 +705,7 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
                     tile_ready(cn);
                     lowest = cn;
                     nz_tile = false;
+                    load_p(l31, lowest, pdn, pun, pln, true, cn);  // the new tile's cells of this sub-group
                 }
             }
             const int l0 = l31 + 31;  // lane 0's column at the first step
@@ -614,25 +716,18 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
             if (l31_on) {
                 const int lo = max(l31 - 7, Jstop);
                 const int zb2 = wait_below(lo, l31);
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) si8[kk] = (l31 - kk >= Jstop) ? s_below(l31 - kk, zb2) : T(0);
+                s_below8(l31, lo, zb2, si8);
             } else {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) si8[kk] = T(0);
             }
-            // probabilities of this sub-group's cells (rotated rows r, uniform)
-            T pd8[8], pu8[8], pl8[8];
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                const int j = l31 - kk + 31 - t;
-                const bool in_run = j >= Jstop && j <= J && j >= 32 * lowest;
-                const int cj = in_run ? (j >> 5) : c;
-                const int r = (l31 - kk + 31) & 31;
-                const T *pt = mypool + ((size_t)q * a.C + cj) * 3 * 1024 + r * 32 + t;
-                pd8[kk] = in_run ? ldcg(pt) : T(0);
-                pu8[kk] = in_run ? ldcg(pt + 1024) : T(0);
-                pl8[kk] = in_run ? ldcg(pt + 2048) : T(0);
+                pd8[kk] = pdn[kk];
+                pu8[kk] = pun[kk];
+                pl8[kk] = pln[kk];
             }
+            load_p(l31 - 8, lowest, pdn, pun, pln, false, 0);  // next sub-group (tiles already ready)
             T so8[8];
             bool nzg = false;
             const bool fixg = a.bw != 0 || (bottom && l31 - 7 <= M - 1 && M - 1 <= l0);
@@ -678,6 +773,7 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
                         for (int kk = 0; kk < 8; ++kk) {
                             const int j = l0 - kk;
                             if (j >= lo0 && j <= J) {
+                                B5_CHECK(j >= 0 && j < M, "spill write", j, lo0);
                                 ring_me[j & (kB5Ring - 1)] = so8[kk];
                                 spill_me[j] = so8[kk];
                             }
@@ -705,6 +801,7 @@ __device__ void b5_strip(Bwd5Shared<T, NE, NH> &sh, const Dp3Args<T> &A, T *mypo
         carry = __any_sync(kFull, e_right != T(0));  // E leaves the drained tile on some row
     }
     // ---- strip done: everything left of chunk c + 1 carries no S upward
+    publish_top(0);  // never swept: the whole strip is dead
     if (t == 0) {
         const int zbme = 32 * (c + 1);
         __threadfence_block();
@@ -755,6 +852,8 @@ __global__ void __launch_bounds__(32 * (NE + NH), 1) sdtw_backward5_kernel(Dp3Ar
             sh.e_pos[e] = INT_MAX;
         }
         for (int e = threadIdx.x; e < kB5JQ; e += blockDim.x) {
+            sh.jobs[0][e] = make_int4(-3, -3, -3, -3);
+            sh.jobs[1][e] = make_int4(-3, -3, -3, -3);
             sh.job_seq[0][e] = 0;
             sh.job_rd[0][e] = e - kB5JQ;
             sh.job_seq[1][e] = 0;

@@ -706,8 +706,25 @@ struct Pipeline {
                     launch_ptr(ctx, kern, persistent_grid(kern, 64 * kW, smem, 2 * B * S), 64 * kW, smem, A, stat,
                                ftc());
                 }
-            } else {
+            } else if (A.knob[3] == 5) {  // experiments: the per-pair pipeline backward
                 launch_backward5(A);
+            } else if (fused) {
+                auto kern = sdtw::k_backward4<T, true, false, 2>();
+                const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);
+                launch_ptr(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat,
+                           sdtw::FusedTcArgs{});
+            } else {
+                // recompute window: 3 tiles per request where alignment bands
+                // are narrow and strips few (C2: 0.447 vs 0.455 ms, C3: 1.63
+                // vs 1.72 ms), 2 (three workers per SM) where bands are wide
+                // or strips many (C1 backward -16 %, C5 -25 %)
+                const bool win2 = gamma >= 0.5 || (size_t)B * S > 8192;
+                auto kern = win2 ? sdtw::k_backward4<T, false, false, 2>() : sdtw::k_backward4<T, false, false, 3>();
+                const size_t smem = (win2 ? sdtw::Bwd4Smem<T, false, false, 2>::kPerWarp
+                                          : sdtw::Bwd4Smem<T, false, false, 3>::kPerWarp) *
+                                    sizeof(T);
+                launch_ptr(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat,
+                           sdtw::FusedTcArgs{});
             }
         }
         if (ctx->trace) {  // diagnostics: the backward's counters (sdtw_debug_counters)
@@ -774,6 +791,10 @@ struct Pipeline {
         spill = Buf<T>(ctx, (size_t)grid * 2 * NE * M);
         int *timeouts = nullptr;
         CUDA_OK(cudaGetSymbolAddress((void **)&timeouts, sdtw::g_sdtw_wait_timeouts));
+        if (A.knob[2]) {  // experiments: bounded waits give up after 2^knob spins
+            if (std::is_same<T, float>::value) sdtw::set_b5_spin_limit_f32(1u << A.knob[2]);
+            else sdtw::set_b5_spin_limit_f64(1u << A.knob[2]);
+        }
         launch_ptr(ctx, kern, grid, 32 * (NE + NH), smem, A, pool.p, spill.p, timeouts);
     }
 
@@ -1341,6 +1362,19 @@ int sdtw_debug_counters(sdtw_ctx *ctx, unsigned *out, int n)
 {
     if (!ctx || !out) return SDTW_EINVAL;
     for (int i = 0; i < n && i < 16; ++i) out[i] = ctx->dbg_counters[i];
+    return SDTW_OK;
+}
+
+int sdtw_debug_phase_status(sdtw_ctx *ctx, int *out, int n)
+{
+    if (!ctx || !out) return SDTW_EINVAL;
+    for (int i = 0; i < n && i < SDTW_NUM_PHASES; ++i) {
+        out[i] = -1;
+        if (ctx->timing && ctx->ev_used[i]) {
+            const cudaError_t e0 = cudaEventQuery(ctx->ev[i][0]), e1 = cudaEventQuery(ctx->ev[i][1]);
+            out[i] = (e0 == cudaSuccess ? 1 : 0) + (e1 == cudaSuccess ? 2 : 0);
+        }
+    }
     return SDTW_OK;
 }
 

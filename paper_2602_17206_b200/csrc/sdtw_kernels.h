@@ -35,6 +35,8 @@ int take_timeouts_bwd4();
 int take_timeouts_bwd5_f32();
 int take_timeouts_bwd5_f64();
 int take_b5_dbg_f32(int *out, int n);
+void set_b5_spin_limit_f32(unsigned v);
+void set_b5_spin_limit_f64(unsigned v);
 int take_b5_dbg_f64(int *out, int n);
 
 }  // namespace sdtw
