@@ -210,6 +210,44 @@ int sdtw_nccl_finalize(sdtw_ctx *ctx);
 int sdtw_allreduce_grad_f32(sdtw_ctx *ctx, float *grad_dev, size_t n,
                             double *value_dev);
 
+/* ---- multi-GPU, one process ----------------------------
+ * G contexts, normally one per device (sdtw_ctx_create(g)).  The batch is
+ * split into G contiguous pair shards [g B / G, (g+1) B / G) (the layout of
+ * backward.hpp:276-304: pairs are independent), shard g runs on ctxs[g]
+ * (its device, stream and allocator) from its own host thread, all shards
+ * concurrently, with no collective; the results are bit for bit those of a
+ * single context (per-pair operand scales).  Host pointers only
+ * (ptr_kind = SDTW_PTR_HOST): each shard stages its own slice.  Replaces the
+ * reference's single-host sdtw_with_gradients (backward.hpp:276-304) when
+ * more than one GPU is visible. */
+/* Number of visible CUDA devices (0 when none). */
+int sdtw_device_count(int *n);
+int sdtw_fwd_bwd_multi_f32(sdtw_ctx *const *ctxs, int G, const float *x,
+                           const float *y, size_t B, size_t N, size_t M,
+                           size_t D, const sdtw_config *cfg, int ptr_kind,
+                           float *loss, float *grad_x, float *grad_y);
+int sdtw_fwd_bwd_multi_f64(sdtw_ctx *const *ctxs, int G, const double *x,
+                           const double *y, size_t B, size_t N, size_t M,
+                           size_t D, const sdtw_config *cfg, int ptr_kind,
+                           double *loss, double *grad_x, double *grad_y);
+/* One NCCL communicator over the G contexts' devices of this process
+ * (ncclCommInitAll); the devices must be distinct. */
+int sdtw_nccl_init_all(sdtw_ctx *const *ctxs, int G);
+/* barycenter_objective (barycenter.hpp:60-86) over G devices: members in
+ * G contiguous shards, each device computes its shard's weighted objective
+ * and grad_z, one NCCL allreduce(sum) of grad_z (fp32) and of the objective
+ * (fp64) over the communicator of sdtw_nccl_init_all (the only collective,
+ * replacing the sequential member loop at barycenter.hpp:77-84); every
+ * device ends with the full sum, which is returned from ctxs[0] (host
+ * pointers).  Deterministic for a fixed G. */
+int sdtw_barycenter_objective_multi_f32(sdtw_ctx *const *ctxs, int G,
+                                        const float *z, size_t Lz,
+                                        const float *members, size_t K,
+                                        size_t L, size_t D, double gamma,
+                                        size_t bandwidth,
+                                        const double *weights, int ptr_kind,
+                                        double *value, float *grad);
+
 #ifdef __cplusplus
 }
 #endif

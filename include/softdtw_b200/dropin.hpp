@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <memory>
 #include <random>
 #include <cmath>
 #include <tuple>
@@ -39,6 +40,18 @@ inline softdtw_b200::Context &context()
 {
     thread_local softdtw_b200::Context ctx(0);
     return ctx;
+}
+
+// Every visible device (one context each) for the pair-sharded hot path;
+// nullptr when only one device is visible.
+inline softdtw_b200::MultiContext *multi_context()
+{
+    thread_local std::unique_ptr<softdtw_b200::MultiContext> mc = [] {
+        int n = 0;
+        sdtw_device_count(&n);
+        return n > 1 ? std::make_unique<softdtw_b200::MultiContext>(n) : nullptr;
+    }();
+    return mc.get();
 }
 
 template <class F>
@@ -250,10 +263,19 @@ SdtwOutput<T> sdtw_with_gradients(const SeriesBatch<T> &x, const SeriesBatch<T> 
     return translate([&] {
         softdtw_b200::Config c = engine_config(cfg);
         c.normalized = false;  // the reference's forward computes the plain loss here
-        ledger_begin(ledger);
-        auto o = context().sdtw_with_gradients(x.raw(), y.raw(), x.batch_size(), x.length(), y.length(),
-                                               x.feature_dim(), c);
-        ledger_end(ledger);
+        // several GPUs: contiguous pair shards, one per device (a ledger
+        // accounts one device's allocations, so a ledger keeps one device)
+        auto *mc = ledger ? nullptr : multi_context();
+        softdtw_b200::Output<T> o;
+        if (mc && x.batch_size() > 1) {
+            o = mc->sdtw_with_gradients<T>(x.raw(), y.raw(), x.batch_size(), x.length(), y.length(),
+                                           x.feature_dim(), c);
+        } else {
+            ledger_begin(ledger);
+            o = context().sdtw_with_gradients(x.raw(), y.raw(), x.batch_size(), x.length(), y.length(),
+                                              x.feature_dim(), c);
+            ledger_end(ledger);
+        }
         for (const T v : o.loss)
             if (!std::isfinite(v))
                 throw softdtw_b200::UnreachableEndError("forward: R[N,M] is not finite (end cell unreachable)");
@@ -292,6 +314,17 @@ std::pair<double, std::vector<T>> barycenter_objective(const SeriesBatch<T> &z, 
                 flat.insert(flat.end(), prob.members[k].raw().begin(), prob.members[k].raw().end());
                 w.push_back(prob.weights.empty() ? 1.0 : prob.weights[k]);
                 ++K;
+            }
+            // several GPUs (fp32): member shards + one NCCL allreduce of grad_z
+            auto *mc = multi_context();
+            if constexpr (std::is_same<T, float>::value) {
+                if (mc && K > 1) {
+                    value += mc->barycenter_objective_into(z.raw().data(), Lz, flat.data(), K, L, D, prob.gamma,
+                                                           prob.bandwidth, w.data(), g.data());
+                    if (lengths.size() == 1) return std::make_pair(value, std::move(g));
+                    for (std::size_t i = 0; i < grad.size(); ++i) grad[i] += g[i];
+                    continue;
+                }
             }
             value += ctx.barycenter_objective_into<T>(z.raw().data(), Lz, flat.data(), K, L, D, prob.gamma,
                                                       prob.bandwidth, w.data(), g.data());

@@ -6,6 +6,7 @@
 // exception taxonomy (types.hpp:17-54).  dropin.hpp adapts these to the
 // reference's own containers.
 #pragma once
+#include <algorithm>
 #include <cstddef>
 #include <stdexcept>
 #include <string>
@@ -229,6 +230,67 @@ class Context {
         return out;
     }
     sdtw_ctx *ctx_ = nullptr;
+};
+
+// One context per visible device: sdtw_with_gradients over
+// contiguous pair shards, all devices concurrently (no collective; bit for
+// bit the single-device result), and the barycenter objective over member
+// shards with one NCCL allreduce of grad_z (ncclCommInitAll, one process).
+class MultiContext {
+  public:
+    // devices 0 .. ndev-1 (ndev < 0: every visible device)
+    explicit MultiContext(int ndev = -1)
+    {
+        if (ndev < 0) check(sdtw_device_count(&ndev));
+        if (ndev < 1) throw Error("no CUDA device available (the engine has no CPU fallback)");
+        for (int d = 0; d < ndev; ++d) ctx_.emplace_back(d);
+        for (auto &c : ctx_) raw_.push_back(c.get());
+    }
+    int devices() const { return (int)ctx_.size(); }
+    Context &operator[](int g) { return ctx_[g]; }
+
+    template <class T>
+    Output<T> sdtw_with_gradients(const std::vector<T> &x, const std::vector<T> &y, std::size_t B, std::size_t N,
+                                  std::size_t M, std::size_t D, const Config &cfg)
+    {
+        if (x.size() != B * N * D || y.size() != B * M * D) throw ValidationError("buffer size mismatch");
+        Output<T> out;
+        out.loss.resize(B);
+        out.grad_x.resize(B * N * D);
+        out.grad_y.resize(B * M * D);
+        const sdtw_config c = cfg.c();
+        const int G = (int)std::min<std::size_t>(raw_.size(), B);
+        if constexpr (sizeof(T) == 4)
+            check(sdtw_fwd_bwd_multi_f32(raw_.data(), G, x.data(), y.data(), B, N, M, D, &c, SDTW_PTR_HOST,
+                                         out.loss.data(), out.grad_x.data(), out.grad_y.data()));
+        else
+            check(sdtw_fwd_bwd_multi_f64(raw_.data(), G, x.data(), y.data(), B, N, M, D, &c, SDTW_PTR_HOST,
+                                         out.loss.data(), out.grad_x.data(), out.grad_y.data()));
+        return out;
+    }
+
+    // fp32 barycenter objective over all devices (one NCCL communicator,
+    // created on first use); a single device takes the one-context path.
+    double barycenter_objective_into(const float *z, std::size_t Lz, const float *members, std::size_t K,
+                                     std::size_t L, std::size_t D, double gamma, std::size_t bandwidth,
+                                     const double *weights, float *grad)
+    {
+        if (raw_.size() == 1)
+            return ctx_[0].barycenter_objective_into<float>(z, Lz, members, K, L, D, gamma, bandwidth, weights, grad);
+        if (!nccl_) {
+            check(sdtw_nccl_init_all(raw_.data(), (int)raw_.size()));
+            nccl_ = true;
+        }
+        double value = 0;
+        check(sdtw_barycenter_objective_multi_f32(raw_.data(), (int)raw_.size(), z, Lz, members, K, L, D, gamma,
+                                                  bandwidth, weights, SDTW_PTR_HOST, &value, grad));
+        return value;
+    }
+
+  private:
+    std::vector<Context> ctx_;
+    std::vector<sdtw_ctx *> raw_;
+    bool nccl_ = false;
 };
 
 }  // namespace softdtw_b200

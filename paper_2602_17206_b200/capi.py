@@ -32,7 +32,8 @@ EXPORTED = [
     "sdtw_forward_backward_E_f32", "sdtw_forward_backward_E_f64", "sdtw_input_grads_f32",
     "sdtw_input_grads_f64", "sdtw_barycenter_objective_f32", "sdtw_barycenter_objective_f64",
     "sdtw_adam_step_f32", "sdtw_adam_step_f64", "sdtw_nccl_get_unique_id", "sdtw_nccl_init",
-    "sdtw_nccl_finalize", "sdtw_allreduce_grad_f32",
+    "sdtw_nccl_finalize", "sdtw_allreduce_grad_f32", "sdtw_fwd_bwd_multi_f32", "sdtw_fwd_bwd_multi_f64",
+    "sdtw_nccl_init_all", "sdtw_barycenter_objective_multi_f32", "sdtw_device_count",
 ]
 
 
@@ -113,6 +114,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sdtw_nccl_init": (I, [P, P, I, I]),
         "sdtw_nccl_finalize": (I, [P]),
         "sdtw_allreduce_grad_f32": (I, [P, P, S, P]),
+        "sdtw_nccl_init_all": (I, [C.POINTER(P), I]),
+        "sdtw_device_count": (I, [C.POINTER(I)]),
+        "sdtw_barycenter_objective_multi_f32": (I, [C.POINTER(P), I, P, S, P, S, S, S, D, S, P, I, P, P]),
     }
     for suf in ("f32", "f64"):
         sig[f"sdtw_fwd_bwd_{suf}"] = (I, [P, P, P, S, S, S, S, cfgp, I, P, P, P])
@@ -122,6 +126,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         sig[f"sdtw_input_grads_{suf}"] = (I, [P, P, P, P, S, S, S, S, I, P, P])
         sig[f"sdtw_barycenter_objective_{suf}"] = (I, [P, P, S, P, S, S, S, D, S, P, I, P, P])
         sig[f"sdtw_adam_step_{suf}"] = (I, [P, P, P, P, P, S, S, D, D, D, D, I])
+        sig[f"sdtw_fwd_bwd_multi_{suf}"] = (I, [C.POINTER(P), I, P, P, S, S, S, S, cfgp, I, P, P, P])
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
         fn.restype = res
@@ -408,3 +413,53 @@ class Engine:
     def allreduce_grad(self, grad_dev, value_dev=None):
         _raise(self.lib.sdtw_allreduce_grad_f32(self.ctx, grad_dev.data_ptr(), grad_dev.numel(),
                                                 None if value_dev is None else value_dev.data_ptr()))
+
+
+# ---- multi-GPU in one process (sdtw_fwd_bwd_multi_*) ------
+def _ctx_array(engines):
+    arr = (C.c_void_p * len(engines))()
+    for g, e in enumerate(engines):
+        arr[g] = e.ctx
+    return arr
+
+
+def sdtw_with_gradients_multi(engines, x, y, gamma=1.0, bandwidth=0, fused=False, dtype=np.float32):
+    """The B pairs in len(engines) contiguous shards, one per engine context
+    (normally one per GPU), run concurrently; host (numpy) arrays only.
+    Bit-identical to one engine's sdtw_with_gradients."""
+    lib = load_library()
+    x = np.ascontiguousarray(x, dtype)
+    y = np.ascontiguousarray(y, dtype)
+    B, N, D = x.shape
+    M = y.shape[1]
+    loss = np.empty(B, dtype)
+    gx = np.empty_like(x)
+    gy = np.empty_like(y)
+    cfg = Engine._cfg(gamma, bandwidth, fused, False)
+    fn = getattr(lib, f"sdtw_fwd_bwd_multi_{Engine._suffix(dtype)}")
+    _raise(fn(_ctx_array(engines), len(engines), x.ctypes.data, y.ctypes.data, B, N, M, D, C.byref(cfg),
+              PTR_HOST, loss.ctypes.data, gx.ctypes.data, gy.ctypes.data))
+    return loss, gx, gy
+
+
+def nccl_init_all(engines):
+    """One NCCL communicator over the engines' devices (ncclCommInitAll)."""
+    _raise(load_library().sdtw_nccl_init_all(_ctx_array(engines), len(engines)))
+
+
+def barycenter_objective_multi(engines, z, members, gamma=1.0, bandwidth=0, weights=None):
+    """barycenter_objective over len(engines) GPUs: member shards + one NCCL
+    allreduce of grad_z and the objective (fp32; host arrays)."""
+    lib = load_library()
+    z = np.ascontiguousarray(z, np.float32)
+    m = np.ascontiguousarray(members, np.float32)
+    Lz, D = z.shape
+    K, L, _ = m.shape
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    grad = np.empty_like(z)
+    val = C.c_double()
+    _raise(lib.sdtw_barycenter_objective_multi_f32(_ctx_array(engines), len(engines), z.ctypes.data, Lz,
+                                                  m.ctypes.data, K, L, D, gamma, bandwidth,
+                                                  None if w is None else w.ctypes.data, PTR_HOST,
+                                                  C.byref(val), grad.ctypes.data))
+    return val.value, grad

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <unordered_map>
 #include <vector>
@@ -153,7 +154,7 @@ struct Nccl {
     typedef int (*InitRank)(void **, int, const void *uid_by_value_dummy, int);
     void *lib = nullptr;
     void *get_uid = nullptr, *init_rank = nullptr, *allreduce = nullptr, *destroy = nullptr,
-         *err_str = nullptr;
+         *err_str = nullptr, *init_all = nullptr, *group_start = nullptr, *group_end = nullptr;
     bool load()
     {
         if (lib) return true;
@@ -164,6 +165,9 @@ struct Nccl {
         allreduce = dlsym(lib, "ncclAllReduce");
         destroy = dlsym(lib, "ncclCommDestroy");
         err_str = dlsym(lib, "ncclGetErrorString");
+        init_all = dlsym(lib, "ncclCommInitAll");
+        group_start = dlsym(lib, "ncclGroupStart");
+        group_end = dlsym(lib, "ncclGroupEnd");
         return get_uid && init_rank && allreduce && destroy;
     }
 };
@@ -1122,6 +1126,25 @@ int input_grads(sdtw_ctx *ctx, const T *E, const T *x, const T *y, size_t B, siz
     });
 }
 
+// Device part of barycenter_objective: all K members as one batch against
+// z broadcast K times, then the weighted member reduction in member order
+// (barycenter.hpp:75-84) into grad (Lz*D) and value (1 double, fp64 sum).
+template <class T>
+void bary_core(sdtw_ctx *ctx, const T *zd, size_t Lz, const T *md, size_t K, size_t L, size_t D,
+               const sdtw_config *cfg, const double *wd, T *grad, double *value)
+{
+    Buf<T> zb(ctx, K * Lz * D);
+    LAUNCH(ctx, sdtw::broadcast_kernel<T>, grid_for(K * Lz * D, 256), 256, 0, zd, Lz * D, (int)K, zb.p);
+    Buf<T> loss(ctx, K), gx(ctx, K * Lz * D);
+    Pipeline<T> pl(ctx, zb.p, md, K, Lz, L, D, cfg);
+    pl.norms();
+    pl.costs();
+    loss_out<T>(pl, loss.p);
+    pl.backward(gx.p, nullptr, false);
+    LAUNCH(ctx, sdtw::member_reduce_kernel<T>, grid_for(Lz * D, 256), 256, 0, gx.p, loss.p, wd, (int)K, Lz * D,
+           grad, value);
+}
+
 // barycenter_objective (barycenter.hpp:60-86): all members in one batch.
 template <class T>
 int bary_objective(sdtw_ctx *ctx, const T *z, size_t Lz, const T *members, size_t K, size_t L,
@@ -1150,20 +1173,205 @@ int bary_objective(sdtw_ctx *ctx, const T *z, size_t Lz, const T *members, size_
             wd = Buf<double>(ctx, K);
             CUDA_OK(cudaMemcpyAsync(wd.p, weights, K * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         }
-        Buf<T> zb(ctx, K * Lz * D);
-        LAUNCH(ctx, sdtw::broadcast_kernel<T>, grid_for(K * Lz * D, 256), 256, 0, zi.p, Lz * D,
-               (int)K, zb.p);
-        Buf<T> loss(ctx, K), gx(ctx, K * Lz * D);
-        Pipeline<T> pl(ctx, zb.p, mi.p, K, Lz, L, D, &cfg);
-        pl.norms();
-        pl.costs();
-        loss_out<T>(pl, loss.p);
-        pl.backward(gx.p, nullptr, false);
-        LAUNCH(ctx, sdtw::member_reduce_kernel<T>, grid_for(Lz * D, 256), 256, 0, gx.p, loss.p,
-               wd.p, (int)K, Lz * D, go.p, vo.p);
+        bary_core<T>(ctx, zi.p, Lz, mi.p, K, L, D, &cfg, wd.p, go.p, vo.p);
         go.finish(ctx);
         vo.finish(ctx);
         finish_call(ctx, ptr_kind);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU in one process: contiguous pair / member
+// shards, one host thread per context (pageable host copies block their
+// thread, so threads are what makes the devices run concurrently).
+// ---------------------------------------------------------------------------
+struct ShardStatus {
+    int code = SDTW_OK;
+    std::string msg;
+    size_t bytes = 0;
+};
+
+template <class Fn>
+int run_shards(sdtw_ctx *const *ctxs, int G, Fn &&fn)
+{
+    if (!ctxs || G < 1) {
+        g_err = "multi-GPU call: need at least one context";
+        return SDTW_EINVAL;
+    }
+    for (int g = 0; g < G; ++g)
+        if (!ctxs[g]) {
+            g_err = "multi-GPU call: null context";
+            return SDTW_EINVAL;
+        }
+    std::vector<ShardStatus> st(G);
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g)
+        th.emplace_back([&, g] {
+            try {
+                DeviceGuard dg(ctxs[g]->device);
+                fn(g, ctxs[g]);
+                CUDA_OK(cudaStreamSynchronize(ctxs[g]->stream));
+            } catch (const SdtwError &e) {
+                st[g] = ShardStatus{e.code, e.msg, e.bytes};
+            } catch (const std::exception &e) {
+                st[g] = ShardStatus{SDTW_ECUDA, e.what(), 0};
+            }
+        });
+    for (auto &t : th) t.join();
+    for (int g = 0; g < G; ++g)
+        if (st[g].code != SDTW_OK) {
+            g_err = "shard " + std::to_string(g) + ": " + st[g].msg;
+            g_oom_bytes = st[g].bytes;
+            return st[g].code;
+        }
+    try {
+        check_wait_timeouts();
+    } catch (const SdtwError &e) {
+        g_err = e.msg;
+        return e.code;
+    }
+    return SDTW_OK;
+}
+
+template <class T>
+int fwd_bwd_multi(sdtw_ctx *const *ctxs, int G, const T *x, const T *y, size_t B, size_t N, size_t M, size_t D,
+                  const sdtw_config *cfg, int ptr_kind, T *loss, T *gx, T *gy)
+{
+    try {
+        validate(B, N, M, D, cfg);
+        if (!loss) fail(SDTW_EINVAL, "loss output is required");
+        if ((ptr_kind & 0xff) != SDTW_PTR_HOST) fail(SDTW_EINVAL, "multi-GPU calls take host pointers");
+        if (cfg->backward_space == SDTW_BWD_LINEAR)
+            fail(SDTW_EINVAL, "linear-space backward is served by sdtw_backward_table_*");
+    } catch (const SdtwError &e) {
+        g_err = e.msg;
+        return e.code;
+    }
+    return run_shards(ctxs, G, [&](int g, sdtw_ctx *c) {
+        const size_t b0 = B * g / G, b1 = B * (g + 1) / G;
+        if (b1 == b0) return;
+        fwd_bwd_run<T>(c, x + b0 * N * D, y + b0 * M * D, b1 - b0, N, M, D, cfg, true, loss + b0,
+                       gx ? gx + b0 * N * D : nullptr, gy ? gy + b0 * M * D : nullptr);
+    });
+}
+
+int nccl_init_all(sdtw_ctx *const *ctxs, int G)
+{
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (!ctxs || G < 1) {
+        g_err = "nccl_init_all: need at least one context";
+        return SDTW_EINVAL;
+    }
+    if (!g_nccl.load() || !g_nccl.init_all) {
+        g_err = "libnccl.so.2 (ncclCommInitAll) not loadable";
+        return SDTW_ENCCL;
+    }
+    std::vector<int> devs(G);
+    for (int g = 0; g < G; ++g) {
+        if (!ctxs[g]) {
+            g_err = "nccl_init_all: null context";
+            return SDTW_EINVAL;
+        }
+        devs[g] = ctxs[g]->device;
+        for (int h = 0; h < g; ++h)
+            if (devs[h] == devs[g]) {
+                g_err = "nccl_init_all: one context per device (NCCL ranks need distinct GPUs)";
+                return SDTW_EINVAL;
+            }
+    }
+    std::vector<void *> comms(G, nullptr);
+    const int rc = ((int (*)(void **, int, const int *))g_nccl.init_all)(comms.data(), G, devs.data());
+    if (rc != 0) {
+        g_err = "ncclCommInitAll failed: " + std::to_string(rc);
+        return SDTW_ENCCL;
+    }
+    for (int g = 0; g < G; ++g) {
+        if (ctxs[g]->nccl_comm && g_nccl.destroy) ((int (*)(void *))g_nccl.destroy)(ctxs[g]->nccl_comm);
+        ctxs[g]->nccl_comm = comms[g];
+        ctxs[g]->nranks = G;
+        ctxs[g]->rank = g;
+    }
+    return SDTW_OK;
+}
+
+template <class T>
+int bary_objective_multi(sdtw_ctx *const *ctxs, int G, const T *z, size_t Lz, const T *members, size_t K,
+                         size_t L, size_t D, double gamma, size_t bw, const double *weights, int ptr_kind,
+                         double *value, T *grad)
+{
+    sdtw_config cfg{gamma, bw, SDTW_COST_UNFUSED, SDTW_BWD_LOG, 0};
+    try {
+        if (K == 0) fail(SDTW_EINVAL, "barycenter: need at least one member series");
+        if (Lz == 0) fail(SDTW_EINVAL, "barycenter: target length must be >= 1");
+        if (weights) {
+            double sum = 0;
+            for (size_t k = 0; k < K; ++k) {
+                if (weights[k] < 0) fail(SDTW_EINVAL, "barycenter: negative weight");
+                sum += weights[k];
+            }
+            if (sum == 0) fail(SDTW_EINVAL, "barycenter: all weights are zero");
+        }
+        validate(K, Lz, L, D, &cfg);
+        if ((ptr_kind & 0xff) != SDTW_PTR_HOST) fail(SDTW_EINVAL, "multi-GPU calls take host pointers");
+        if (!grad || !value) fail(SDTW_EINVAL, "value and grad outputs are required");
+        if (!ctxs || G < 1) fail(SDTW_EINVAL, "multi-GPU call: need at least one context");
+        for (int g = 0; g < G; ++g)
+            if (!ctxs[g] || !ctxs[g]->nccl_comm || ctxs[g]->nranks != G || ctxs[g]->rank != g)
+                fail(SDTW_ENCCL, "barycenter multi: run sdtw_nccl_init_all on these contexts first");
+    } catch (const SdtwError &e) {
+        g_err = e.msg;
+        return e.code;
+    }
+    // per-device partial objective and gradient, left on the device
+    std::vector<Buf<T>> gdev(G);
+    std::vector<Buf<double>> vdev(G);
+    int rc = run_shards(ctxs, G, [&](int g, sdtw_ctx *c) {
+        const size_t k0 = K * g / G, k1 = K * (g + 1) / G;
+        gdev[g] = Buf<T>(c, Lz * D);
+        vdev[g] = Buf<double>(c, 1);
+        if (k1 == k0) {  // empty shard: contributes zeros
+            CUDA_OK(cudaMemsetAsync(gdev[g].p, 0, Lz * D * sizeof(T), c->stream));
+            CUDA_OK(cudaMemsetAsync(vdev[g].p, 0, sizeof(double), c->stream));
+            return;
+        }
+        In<T> zi(c, z, Lz * D, true), mi(c, members + k0 * L * D, (k1 - k0) * L * D, true);
+        Buf<double> wd;
+        if (weights) {
+            wd = Buf<double>(c, k1 - k0);
+            CUDA_OK(cudaMemcpyAsync(wd.p, weights + k0, (k1 - k0) * sizeof(double), cudaMemcpyHostToDevice,
+                                    c->stream));
+        }
+        bary_core<T>(c, zi.p, Lz, mi.p, k1 - k0, L, D, &cfg, wd.p, gdev[g].p, vdev[g].p);
+        // inputs are released at scope exit: finish their reads first
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+    });
+    if (rc != SDTW_OK) return rc;
+    // the only collective: sum of grad_z (fp32) and of the objective (fp64)
+    {
+        std::lock_guard<std::mutex> lk(g_nccl_mu);
+        typedef int (*AR)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+        AR ar = (AR)g_nccl.allreduce;
+        const int dt = sizeof(T) == 4 ? 7 : 8;  // ncclFloat32 / ncclFloat64 (nccl.h)
+        ((int (*)())g_nccl.group_start)();
+        int nrc = 0;
+        for (int g = 0; g < G && nrc == 0; ++g) {
+            DeviceGuard dg(ctxs[g]->device);
+            nrc = ar(gdev[g].p, gdev[g].p, Lz * D, dt, 0, ctxs[g]->nccl_comm, ctxs[g]->stream);
+            if (nrc == 0) nrc = ar(vdev[g].p, vdev[g].p, 1, 8, 0, ctxs[g]->nccl_comm, ctxs[g]->stream);
+        }
+        const int erc = ((int (*)())g_nccl.group_end)();
+        if (nrc != 0 || erc != 0) {
+            g_err = "ncclAllReduce failed: " + std::to_string(nrc ? nrc : erc);
+            return SDTW_ENCCL;
+        }
+    }
+    return guarded(ctxs[0], [&] {
+        CUDA_OK(cudaMemcpyAsync(grad, gdev[0].p, Lz * D * sizeof(T), cudaMemcpyDeviceToHost, ctxs[0]->stream));
+        CUDA_OK(cudaMemcpyAsync(value, vdev[0].p, sizeof(double), cudaMemcpyDeviceToHost, ctxs[0]->stream));
+        for (int g = 0; g < G; ++g) {
+            DeviceGuard dg(ctxs[g]->device);
+            CUDA_OK(cudaStreamSynchronize(ctxs[g]->stream));
+        }
     });
 }
 
@@ -1475,6 +1683,38 @@ int sdtw_adam_step_f64(sdtw_ctx *ctx, double *z, const double *grad, double *m1,
                        int ptr_kind)
 {
     return adam_step<double>(ctx, z, grad, m1, m2, n, t, lr, b1, b2, eps, ptr_kind);
+}
+
+// ---- multi-GPU (one process) --------------------------------------------
+int sdtw_device_count(int *n)
+{
+    if (!n) return SDTW_EINVAL;
+    if (cudaGetDeviceCount(n) != cudaSuccess) {
+        cudaGetLastError();
+        *n = 0;
+    }
+    return SDTW_OK;
+}
+int sdtw_fwd_bwd_multi_f32(sdtw_ctx *const *ctxs, int G, const float *x, const float *y, size_t B, size_t N,
+                           size_t M, size_t D, const sdtw_config *cfg, int ptr_kind, float *loss, float *gx,
+                           float *gy)
+{
+    return fwd_bwd_multi<float>(ctxs, G, x, y, B, N, M, D, cfg, ptr_kind, loss, gx, gy);
+}
+int sdtw_fwd_bwd_multi_f64(sdtw_ctx *const *ctxs, int G, const double *x, const double *y, size_t B, size_t N,
+                           size_t M, size_t D, const sdtw_config *cfg, int ptr_kind, double *loss, double *gx,
+                           double *gy)
+{
+    return fwd_bwd_multi<double>(ctxs, G, x, y, B, N, M, D, cfg, ptr_kind, loss, gx, gy);
+}
+int sdtw_nccl_init_all(sdtw_ctx *const *ctxs, int G) { return nccl_init_all(ctxs, G); }
+int sdtw_barycenter_objective_multi_f32(sdtw_ctx *const *ctxs, int G, const float *z, size_t Lz,
+                                        const float *members, size_t K, size_t L, size_t D, double gamma,
+                                        size_t bandwidth, const double *weights, int ptr_kind, double *value,
+                                        float *grad)
+{
+    return bary_objective_multi<float>(ctxs, G, z, Lz, members, K, L, D, gamma, bandwidth, weights, ptr_kind,
+                                       value, grad);
 }
 
 // ---- NCCL (barycenter gradient allreduce) ---------------------------------
