@@ -11,7 +11,7 @@
 //   sdtw_with_gradients<T>(x, y, cfg, threads, ledger)   backward.hpp:276-304
 //   barycenter_objective<T>(z, prob)                     barycenter.hpp:60-86
 //   solve_barycenter<T>(prob, init, opts, index, user_z) barycenter.hpp:159-211
-//   run_bench_row(row, threads, seed, mem_limit)         bench.hpp:52-107
+// (run_bench_row, bench.hpp:52-107, is in softdtw_b200/bench.hpp)
 // Standalone tables (DpTableBatch / GradTableBatch / CostMatrixBatch /
 // NormCache) are the reference's own host containers, filled from the
 // engine's device results, so callers read them with .at() as before; the
@@ -374,57 +374,6 @@ BarycenterTrace<T> solve_barycenter(const BarycenterProblem<T> &prob,
         }
     }
     return trace;
-}
-
-// run_bench_row (bench.hpp:52-107): the reference's benchmark row on the
-// engine — same generator (mt19937_64(seed), N(0,1) fp32, all of x then all
-// of y), same timing (steady_clock around the complete sdtw_with_gradients
-// call, host buffers in and out), same ledger semantics (device peak of the
-// last timed run).  Failures are recorded in the row, not thrown.
-inline BenchResultRow run_bench_row(const BenchConfigRow &row, unsigned threads = 0, std::uint64_t seed = 42,
-                                    std::size_t mem_limit_bytes = 0)
-{
-    validate_bench_row(row);
-    BenchResultRow out;
-    out.config = row;
-    try {
-        std::mt19937_64 rng(seed);
-        std::normal_distribution<float> dist(0.0f, 1.0f);
-        const std::size_t count = row.batch * row.length * row.feature_dim;
-        std::vector<float> xs(count), ys(count);
-        for (auto &v : xs) v = dist(rng);
-        for (auto &v : ys) v = dist(rng);
-        SeriesBatch<float> x(std::move(xs), row.batch, row.length, row.feature_dim);
-        SeriesBatch<float> y(std::move(ys), row.batch, row.length, row.feature_dim);
-        SdtwConfig cfg;
-        cfg.gamma = row.gamma;
-        cfg.cost_mode = row.cost_mode;
-        cfg.backward_space = row.backward_space;
-        AllocationLedger ledger;
-        ledger.limit_bytes = mem_limit_bytes;
-        std::vector<double> times_ms;
-        for (std::size_t it = 0; it < row.warmup + row.repeats; ++it) {
-            ledger.reset();
-            const auto t0 = std::chrono::steady_clock::now();
-            auto result = b200::sdtw_with_gradients(x, y, cfg, threads, &ledger);
-            const auto t1 = std::chrono::steady_clock::now();
-            out.loss0 = result.loss[0];
-            if (it >= row.warmup) times_ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
-            out.peak_ledger_bytes = ledger.peak_bytes;
-        }
-        double mean = 0;
-        for (double t : times_ms) mean += t;
-        mean /= double(times_ms.size());
-        double var = 0;
-        for (double t : times_ms) var += (t - mean) * (t - mean);
-        out.mean_runtime_ms = mean;
-        out.std_runtime_ms = std::sqrt(var / double(times_ms.size()));
-        out.ok = true;
-    } catch (const std::exception &ex) {
-        out.ok = false;
-        out.error = ex.what();
-    }
-    return out;
 }
 
 }  // namespace b200

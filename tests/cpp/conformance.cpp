@@ -11,6 +11,7 @@
 #include <random>
 
 #include "softdtw_b200/dropin.hpp"
+#include "softdtw_b200/bench.hpp"
 
 using namespace softdtw;
 

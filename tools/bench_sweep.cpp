@@ -3,8 +3,10 @@
 // (softdtw::b200::run_bench_row), over the paper's Fig. 1 axes at B = 32
 // (SURVEY.md §8(d)): L in {128 .. 4096} at D = 128 and D in {16 .. 1024} at
 // L = 256, both cost modes, log space.  Columns: the reference's own, then
-// DP cells/s (B L^2 / mean time, end to end with host buffers), the GPU
-// count, the host core count and the device peak in MB.
+// DP cells/s (B L^2 / mean time, end to end with host buffers), DP cells/s on
+// the device (the fwd+bwd kernels alone) and that rate as a fraction of the
+// SFU roofline (7 MUFU per cell), the GPU count, the host core count and the
+// device peak in MB (softdtw::b200::measure_row, softdtw_b200/bench.hpp).
 //
 //   tools/_bin/bench_sweep [--quick] [--repeats R] [--gamma G] > sweep.csv
 #include <softdtw/softdtw.hpp>
@@ -16,6 +18,7 @@
 #include <vector>
 
 #include "softdtw_b200/dropin.hpp"
+#include "softdtw_b200/bench.hpp"
 
 using namespace softdtw;
 
@@ -37,7 +40,8 @@ int main(int argc, char **argv)
     for (auto L : Ls) shapes.emplace_back(L, 128);
     for (auto D : Ds)
         if (D != 128) shapes.emplace_back(256, D);
-    std::printf("%s,cells_per_s,gpus,host_cores,device_peak_mb\n", bench_csv_header().c_str());
+    std::printf("%s,cells_per_s,device_cells_per_s,sfu_roofline_fraction,gpus,host_cores,device_peak_mb\n",
+                bench_csv_header().c_str());
     for (auto [L, D] : shapes) {
         for (CostMode mode : {CostMode::unfused, CostMode::fused}) {
             BenchConfigRow row;
@@ -48,11 +52,11 @@ int main(int argc, char **argv)
             row.cost_mode = mode;
             row.repeats = repeats;
             row.warmup = 1;
-            const BenchResultRow r = b200::run_bench_row(row);
-            const double cells = double(row.batch) * double(L) * double(L);
-            std::printf("%s,%.6g,1,%u,%.1f\n", bench_csv_row(r).c_str(),
-                        r.ok ? cells / (r.mean_runtime_ms * 1e-3) : 0.0, std::thread::hardware_concurrency(),
-                        double(r.peak_ledger_bytes) / (1 << 20));
+            const b200::EngineBenchRow e = b200::measure_row(row);
+            const BenchResultRow &r = e.row;
+            std::printf("%s,%.6g,%.6g,%.4f,1,%u,%.1f\n", bench_csv_row(r).c_str(), r.ok ? e.cells_per_s : 0.0,
+                        r.ok ? e.device_cells_per_s : 0.0, r.ok ? e.sfu_fraction : 0.0,
+                        std::thread::hardware_concurrency(), double(r.peak_ledger_bytes) / (1 << 20));
             std::fflush(stdout);
         }
     }
