@@ -431,11 +431,13 @@ struct Pipeline {
         KK = ((M + 62) / 32) * 32;
         dpad = ((D + 63) / 64) * 64;
         tc_fused = fused && std::is_same<T, float>::value && dpad <= sdtw::kFtcMaxD;
-        // fp32 with D > 128: the fused tensor-core kernels stage at most 128
-        // features per operand row, so the call runs the unfused schedule
-        // (tensor-core cost tensor; identical costs, the tensor is
-        // materialised).  fp64 fused mode keeps per-cell SIMT costs.
-        if (fused && std::is_same<T, float>::value && !tc_fused) fused = false;
+        // fp32 fused mode with D > 128 (and fp64 fused mode): the fused
+        // tensor-core kernels stage at most 128 features per operand row, so
+        // these compute each cost inside the DP kernels with an fp32 (fp64)
+        // SIMT dot product (cost.hpp:63-78 order): still no cost tensor, so
+        // the peak stays below unfused by the whole B x N x M tensor, but the
+        // fp32 costs then round differently from the tensor-core unfused
+        // ones (within the parity tolerances, not bit for bit).
     }
 
     // fp32 fused mode with D <= 128 runs on the tensor cores (sdtw_fused.cuh);

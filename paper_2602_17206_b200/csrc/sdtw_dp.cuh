@@ -54,7 +54,26 @@ __device__ __forceinline__ T cost_cell(const T *__restrict__ xr, const T *__rest
                                        T xn, T yn, int D)
 {
     T dot = T(0);
-    for (int kk = 0; kk < D; ++kk) dot = fma(xr[kk], yr[kk], dot);
+    if constexpr (sizeof(T) == 4) {
+        // fp32 (fused mode with D > 128): four independent partial sums
+        // over 16-byte loads when rows are aligned, then (p0 + p1) + (p2 + p3)
+        if ((D & 3) == 0 && ((reinterpret_cast<uintptr_t>(xr) | reinterpret_cast<uintptr_t>(yr)) & 15) == 0) {
+            float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+            for (int kk = 0; kk < D; kk += 4) {
+                const float4 a = __ldg(reinterpret_cast<const float4 *>(xr + kk));
+                const float4 c = __ldg(reinterpret_cast<const float4 *>(yr + kk));
+                p0 = fmaf(a.x, c.x, p0);
+                p1 = fmaf(a.y, c.y, p1);
+                p2 = fmaf(a.z, c.z, p2);
+                p3 = fmaf(a.w, c.w, p3);
+            }
+            dot = (p0 + p1) + (p2 + p3);
+        } else {
+            for (int kk = 0; kk < D; ++kk) dot = fma(xr[kk], yr[kk], dot);
+        }
+    } else {
+        for (int kk = 0; kk < D; ++kk) dot = fma(xr[kk], yr[kk], dot);
+    }
     const T v = (xn - T(2) * dot) + yn;
     return v < T(0) ? T(0) : v;
 }

@@ -309,6 +309,20 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                     if (t < n) halo_s[(kb + t) & 31] = hv;
                     __syncwarp();
                 }
+                // fused mode: the sub-group's costs up front, 8 independent
+                // SIMT dot products per strip (they do not depend on the DP
+                // state, so they leave the step chain; same values)
+                T dk[K][8];
+                if (kFused) {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+                        for (int q = 0; q < K; ++q) {
+                            const int col = kb + kk - 32 * q - t;
+                            const bool active = row_ok[q] && col >= 0 && col < a.M;
+                            dk[q][kk] = active ? load_cost<T, true>(a, b, s0 + q, t, row[q], col + 1) : T(0);
+                        }
+                }
                 // Lean sub-group (one strip per warp, unfused): every lane's
                 // cell is interior and active (col in [1, M), full strip),
                 // not strip 0 (no row-1 selects) and no lane meets its
@@ -321,6 +335,9 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                 if (lean) {
                     const T *rgk = ring + (G & 1) * 1024 + k8 * 32 + t;
                     typename TG::Ent *hp = A.hbt + ((size_t)b * a.S + s0) * a.M + (kb - 31);
+                    // lane 31's h leave after the sub-group (the strip below
+                    // consumes 8 columns at a time: no added lag)
+                    T hb[8];
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
                         const int kl = k8 + kk;
@@ -332,8 +349,13 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                         vck[0] = (kl == ((t - 1) & 31)) ? v : vck[0];
                         l_carry[0] = v;
                         h_prev[0] = h;
-                        TG::store_if(hp + kk, h, epoch, t == 31);
+                        hb[kk] = h;
                     }
+                    if (t == 31) {
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) TG::store(hp + kk, hb[kk], epoch);
+                    }
+                    __syncwarp();
                 } else if (fixup || tail) {
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
@@ -351,7 +373,7 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                             const bool active = row_ok[q] && col >= 0 && col < a.M;
                             T d;
                             if (kFused) {
-                                d = active ? load_cost<T, true>(a, b, s0 + q, t, row[q], col + 1) : T(0);
+                                d = dk[q][kk];
                             } else {
                                 d = ring[(q * 2 + ((G - q) & 1)) * 1024 + kl * 32 + t];
                             }
@@ -401,7 +423,7 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                             const bool active = row_ok[q] && col >= 0 && col < a.M;
                             T d;
                             if (kFused) {
-                                d = active ? load_cost<T, true>(a, b, s0 + q, t, row[q], col + 1) : T(0);
+                                d = dk[q][kk];
                             } else {
                                 d = ring[(q * 2 + ((G - q) & 1)) * 1024 + kl * 32 + t];
                             }

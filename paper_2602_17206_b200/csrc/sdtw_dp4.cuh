@@ -403,7 +403,14 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                     for (int z = 0; z < kWin; ++z) {
                         hs8[z][kk] = halo_s[z * 32 + (q & 31)];
                         // skewed row 32 (cr - z) + q of the ring
-                        d8[z][kk] = kFused ? T(0) : ring[((cr - z + (q >> 5)) & 3) * 1024 + (q & 31) * 32 + t];
+                        // (fused: the SIMT cost up front, off the step chain)
+                        if (kFused) {
+                            const int jj = q - t, wz = z == 0 ? wr : 32;
+                            const bool act = z < nt && row_ok && jj >= 0 && jj < wz;
+                            d8[z][kk] = act ? bwd_cost<T, kFused>(a, ring, b, s, t, i, 32 * (cr - z) + 1 + jj) : T(0);
+                        } else {
+                            d8[z][kk] = ring[((cr - z + (q >> 5)) & 3) * 1024 + (q & 31) * 32 + t];
+                        }
                     }
                 }
                 auto rsteps = [&](auto fix_tag) {
@@ -422,7 +429,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                             const int wz = z == 0 ? wr : 32;
                             const bool act = z < nt && row_ok && jj >= 0 && jj < wz;
                             const int j = 32 * (cr - z) + 1 + jj;
-                            const T d = kFused ? (act ? bwd_cost<T, kFused>(a, ring, b, s, t, i, j) : T(0)) : d8[z][kk];
+                            const T d = d8[z][kk];
                             T v, h, pd, pu, pl;
                             if constexpr (kFix) {
                                 const Cell<T> cc = dp_cell<T, true>(i, j, a.bw, d, u[z], lc[z], a.k, a.gln2);

@@ -417,6 +417,10 @@ for (int k8 = 0; k8 < 32; k8 += 8) {
         }
         typename TG::Ent *hp = hb_me + (kb - 31);
         const unsigned pos0 = base + (unsigned)(kb - 31);
+        // lane 31's eight bottom-row h leave after the sub-group, not one
+        // predicated store pair per step on the step's issue path: the strip
+        // below consumes them 8 columns at a time anyway (no added lag)
+        float hb[8];
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
             const int kl = k8 + kk;
@@ -427,11 +431,19 @@ for (int k8 = 0; k8 < 32; k8 += 8) {
             vck = (kl == ((t - 1) & 31)) ? v : vck;
             l_carry = v;
             h_prev = h;
-            TG::store_if(hp + kk, h, epoch, t == 31);
-            const unsigned pos = pos0 + (unsigned)kk;
-            st_shared_u64_if(hx_me + (pos & (kFtcHx - 1)), ((unsigned long long)pos << 32) | __float_as_uint(h),
-                             pub_local && t == 31);
+            hb[kk] = h;
         }
+        if (t == 31) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                TG::store(hp + kk, hb[kk], epoch);
+                const unsigned pos = pos0 + (unsigned)kk;
+                if (pub_local)
+                    st_shared_u64_if(hx_me + (pos & (kFtcHx - 1)),
+                                     ((unsigned long long)pos << 32) | __float_as_uint(hb[kk]), true);
+            }
+        }
+        __syncwarp();
     } else if (fixup || tail) {
         steps8(std::true_type{});
     } else {

@@ -201,17 +201,19 @@ def test_mem_limit_oom(engine):
     engine.sdtw_with_gradients(x, y, 1.0)
 
 
-def test_fused_uses_less_memory(engine):
-    """acceptance criterion 6 analogue: fused peak well below unfused
-    (B=32, L=512, D=64)."""
-    x, y = _bench_like(32, 512, 64)
+@pytest.mark.parametrize("B,L,D", [(32, 512, 64), (8, 512, 256), (4, 384, 1024)])
+def test_fused_uses_less_memory(engine, B, L, D):
+    """acceptance criterion 6 analogue: fused peak below unfused by at least
+    the B x N x M cost tensor, at every D (D > 128: SIMT costs in the DP
+    kernels, still no cost tensor)."""
+    x, y = _bench_like(B, L, D)
     engine.trim()
     peaks = {}
     for fused in (False, True):
         engine.reset_peak()
         engine.sdtw_with_gradients(x, y, 1.0, fused=fused)
         peaks[fused] = engine.mem_stats()[1]
-    assert peaks[False] - peaks[True] >= 4 * 32 * 512 * 512
+    assert peaks[False] - peaks[True] >= 4 * B * L * L, (peaks, 4 * B * L * L)
 
 
 def test_barycenter_objective_golden(engine, bary_golden):
