@@ -96,12 +96,6 @@ int sdtw_phase_times(sdtw_ctx *ctx, float *ms, int n);
 /* Diagnostics: when trace_dev (device, 2 * B * S uint64) is non-NULL, the
  * forward DP records %globaltimer at each strip's start and end. */
 int sdtw_debug_set_trace(sdtw_ctx *ctx, void *trace_dev);
-/* Diagnostics: with a trace buffer set, the last backward's counters
- * (sdtw_bwd5.cuh: jobs, recomputed tiles, wait cycles ...), n <= 16. */
-int sdtw_debug_counters(sdtw_ctx *ctx, unsigned *out, int n);
-/* Diagnostics: the backward's timed-out dependency waits since the last
- * call, out[0] = count, then (site, CTA, a, b) records; returns the count. */
-int sdtw_debug_waits(int dtype64, int *out, int n);
 /* Diagnostics (timing enabled): per phase 0 = not started, 1 = started,
  * 3 = finished (non-blocking event queries; -1 = phase did not run). */
 int sdtw_debug_phase_status(sdtw_ctx *ctx, int *out, int n);

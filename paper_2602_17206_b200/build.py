@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsdtw_b200.so")
 # the host side (sdtw_capi.cu) and the DP kernels in their own translation
 # units (sdtw_kernels.h), compiled in parallel and linked into one library
-SOURCES = ["sdtw_capi.cu", "k_fwd_f32.cu", "k_fwd_f64.cu", "k_bwd4.cu", "k_bwd5_f32.cu", "k_bwd5_f64.cu",
+SOURCES = ["sdtw_capi.cu", "k_fwd_f32.cu", "k_fwd_f64.cu", "k_bwd4.cu",
            "k_gemm.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 OBJDIR = os.path.join(HERE, "_obj")

@@ -26,7 +26,7 @@ EXPORTED = [
     "sdtw_ctx_create", "sdtw_ctx_destroy", "sdtw_ctx_set_stream", "sdtw_ctx_stream",
     "sdtw_ctx_synchronize", "sdtw_mem_stats", "sdtw_mem_reset_peak", "sdtw_set_mem_limit",
     "sdtw_mem_trim", "sdtw_launch_count", "sdtw_reset_launch_count", "sdtw_ctx_enable_timing",
-    "sdtw_phase_times", "sdtw_debug_set_trace", "sdtw_debug_counters", "sdtw_debug_waits", "sdtw_debug_phase_status", "sdtw_last_error",
+    "sdtw_phase_times", "sdtw_debug_set_trace", "sdtw_debug_phase_status", "sdtw_last_error",
     "sdtw_last_oom_bytes", "sdtw_fwd_bwd_f32", "sdtw_fwd_bwd_f64", "sdtw_forward_f32",
     "sdtw_forward_f64", "sdtw_backward_table_f32", "sdtw_backward_table_f64",
     "sdtw_forward_backward_E_f32", "sdtw_forward_backward_E_f64", "sdtw_input_grads_f32",
@@ -106,8 +106,6 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sdtw_ctx_enable_timing": (I, [P, I]),
         "sdtw_phase_times": (I, [P, C.POINTER(C.c_float), I]),
         "sdtw_debug_set_trace": (I, [P, P]),
-        "sdtw_debug_counters": (I, [P, C.POINTER(C.c_uint), I]),
-        "sdtw_debug_waits": (I, [I, C.POINTER(C.c_int), I]),
         "sdtw_debug_phase_status": (I, [P, C.POINTER(C.c_int), I]),
         "sdtw_last_oom_bytes": (S, []),
         "sdtw_nccl_get_unique_id": (I, [P]),

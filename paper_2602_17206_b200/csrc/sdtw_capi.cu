@@ -31,7 +31,6 @@
 #include "sdtw_dp2.cuh"
 #include "sdtw_dp3.cuh"
 #include "sdtw_dp4.cuh"
-#include "sdtw_bwd5.cuh"
 #include "sdtw_kernels.h"
 #include "sdtw_fused.cuh"
 #include "sdtw_grad.cuh"
@@ -197,7 +196,6 @@ struct sdtw_ctx {
     unsigned long long halo_sig[5] = {};
     unsigned epoch = 0;
     unsigned long long *trace = nullptr;  // debug: per-strip forward timestamps
-    unsigned dbg_counters[16] = {};       // debug: the last backward's counters
     cudaEvent_t ev[SDTW_NUM_PHASES][2] = {};
     bool ev_used[SDTW_NUM_PHASES] = {};
     // Host-pointer calls split the batch into pair chunks, each on its own
@@ -377,8 +375,7 @@ void check_wait_timeouts()
         const int zero = 0;
         cudaMemcpyToSymbol(sdtw::g_sdtw_wait_timeouts, &zero, sizeof(int));
     }
-    n += sdtw::take_timeouts_fwd_f32() + sdtw::take_timeouts_fwd_f64() + sdtw::take_timeouts_bwd4() +
-         sdtw::take_timeouts_bwd5_f32() + sdtw::take_timeouts_bwd5_f64();
+    n += sdtw::take_timeouts_fwd_f32() + sdtw::take_timeouts_fwd_f64() + sdtw::take_timeouts_bwd4();
     if (n != 0) {
         fail(SDTW_ECUDA, "internal: " + std::to_string(n) + " wavefront dependency wait(s) timed out");
     }
@@ -605,8 +602,6 @@ struct Pipeline {
         A.tile_quota = tile_quota;
         A.stats = stats.p;
         A.trace = ctx->trace;
-        if (const char *e = std::getenv("SDTW_KNOBS"))  // experiments only
-            std::sscanf(e, "%d,%d,%d,%d", &A.knob[0], &A.knob[1], &A.knob[2], &A.knob[3]);
         return A;
     }
 
@@ -712,8 +707,6 @@ struct Pipeline {
                     launch_ptr(ctx, kern, persistent_grid(kern, 64 * kW, smem, 2 * B * S), 64 * kW, smem, A, stat,
                                ftc());
                 }
-            } else if (A.knob[3] == 5) {  // experiments: the per-pair pipeline backward
-                launch_backward5(A);
             } else if (fused) {
                 auto kern = sdtw::k_backward4<T, true, false, 2>();
                 const size_t smem = sdtw::Bwd4Smem<T, true>::kPerWarp * sizeof(T);
@@ -732,11 +725,6 @@ struct Pipeline {
                 launch_ptr(ctx, kern, persistent_grid(kern, 64, smem, 2 * B * S), 64, smem, A, stat,
                            sdtw::FusedTcArgs{});
             }
-        }
-        if (ctx->trace) {  // diagnostics: the backward's counters (sdtw_debug_counters)
-            CUDA_OK(cudaMemcpyAsync(ctx->dbg_counters, stats.p, sizeof ctx->dbg_counters, cudaMemcpyDeviceToHost,
-                                    ctx->stream));
-            CUDA_OK(cudaStreamSynchronize(ctx->stream));
         }
         if (gx || gy) {
             // ordered, atomic-free contraction of the stored tiles
@@ -776,32 +764,6 @@ struct Pipeline {
         }
         // the cost tensor is dropped after the backward (backward.hpp:291)
         dsk = Buf<T>();
-    }
-
-    // The per-pair pipeline backward (sdtw_bwd5.cuh): one CTA per pair, E
-    // warps + recompute helpers, P tiles in a per-CTA pool.
-    Buf<T> pool, spill;
-    void launch_backward5(sdtw::Dp3Args<T> &A)
-    {
-        constexpr int NE = 4, NH = 12;
-        using Sh = sdtw::Bwd5Shared<T, NE, NH>;
-        const size_t smem = sizeof(Sh);
-        auto kern = fused ? sdtw::k_backward5<T, 1, NE, NH>() : sdtw::k_backward5<T, 0, NE, NH>();
-        ensure_smem_attr(ctx->device, (const void *)kern, (int)smem);
-        int occ = 0;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * (NE + NH), smem));
-        if (occ < 1) fail(SDTW_ECUDA, "backward5 does not fit on an SM");
-        const int grid = std::max(1, std::min(B, occ * ctx->sm_count));
-        if (C > sdtw::kB5MaxC) fail(SDTW_EINVAL, "backward: M > 131072 columns is not supported");
-        pool = Buf<T>(ctx, (size_t)grid * sdtw::kB5NQ * C * 3 * 1024);
-        spill = Buf<T>(ctx, (size_t)grid * 2 * NE * M);
-        int *timeouts = nullptr;
-        CUDA_OK(cudaGetSymbolAddress((void **)&timeouts, sdtw::g_sdtw_wait_timeouts));
-        if (A.knob[2]) {  // experiments: bounded waits give up after 2^knob spins
-            if (std::is_same<T, float>::value) sdtw::set_b5_spin_limit_f32(1u << A.knob[2]);
-            else sdtw::set_b5_spin_limit_f64(1u << A.knob[2]);
-        }
-        launch_ptr(ctx, kern, grid, 32 * (NE + NH), smem, A, pool.p, spill.p, timeouts);
     }
 
     void grads(T *gx, T *gy)
@@ -1568,13 +1530,6 @@ int sdtw_debug_set_trace(sdtw_ctx *ctx, void *trace_dev)
     return SDTW_OK;
 }
 
-int sdtw_debug_counters(sdtw_ctx *ctx, unsigned *out, int n)
-{
-    if (!ctx || !out) return SDTW_EINVAL;
-    for (int i = 0; i < n && i < 16; ++i) out[i] = ctx->dbg_counters[i];
-    return SDTW_OK;
-}
-
 int sdtw_debug_phase_status(sdtw_ctx *ctx, int *out, int n)
 {
     if (!ctx || !out) return SDTW_EINVAL;
@@ -1588,10 +1543,6 @@ int sdtw_debug_phase_status(sdtw_ctx *ctx, int *out, int n)
     return SDTW_OK;
 }
 
-int sdtw_debug_waits(int dtype64, int *out, int n)
-{
-    return dtype64 ? sdtw::take_b5_dbg_f64(out, n) : sdtw::take_b5_dbg_f32(out, n);
-}
 
 const char *sdtw_last_error(void) { return g_err.c_str(); }
 size_t sdtw_last_oom_bytes(void) { return g_oom_bytes; }

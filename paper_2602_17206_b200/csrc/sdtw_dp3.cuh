@@ -125,7 +125,6 @@ struct Dp3Args {
     int tile_quota;
     unsigned *stats;               // [0] live tiles, [1] tiles stored, [2] overflow (in-warp)
     unsigned long long *trace;     // optional [B*S][2] %globaltimer at strip start / end (forward)
-    int knob[4];                   // experiment knobs (0 = default)
 };
 
 __device__ __forceinline__ unsigned long long global_ns()

@@ -20,9 +20,6 @@ KFn<Dp3Args<float>, FusedTcArgs> k_forward_tc();
 // k_bwd4.cu
 template <class T, bool kFused, bool kTc, int kWin>
 KFn<Dp3Args<T>, unsigned long long *, FusedTcArgs> k_backward4();
-// k_bwd5_f32.cu / k_bwd5_f64.cu
-template <class T, int kCost, int NE, int NH>
-KFn<Dp3Args<T>, T *, T *, int *> k_backward5();
 // k_gemm.cu
 KFn<const uint8_t *, const uint8_t *, const float *, const float *, const unsigned *, int, int, int, int, int, int,
     int, int, float *>
@@ -32,12 +29,6 @@ k_cost_gemm();
 int take_timeouts_fwd_f32();
 int take_timeouts_fwd_f64();
 int take_timeouts_bwd4();
-int take_timeouts_bwd5_f32();
-int take_timeouts_bwd5_f64();
-int take_b5_dbg_f32(int *out, int n);
-void set_b5_spin_limit_f32(unsigned v);
-void set_b5_spin_limit_f64(unsigned v);
-int take_b5_dbg_f64(int *out, int n);
 
 }  // namespace sdtw
 
