@@ -1,6 +1,8 @@
 // b200_redirect.hpp — the reference's own headers with its hot-path
-// functions served by the B200 engine (test infrastructure for running the
-// reference's unit suite unchanged against the drop-in).
+// functions served by the B200 engine: the same-name drop-in.  Code written
+// against the reference (its unit suite, its CLI tools/sdtw.cpp, a user's
+// program) compiles unchanged and runs on the GPU when include/softdtw_redirect
+// comes first on the include path and it links libsdtw_b200.so.
 //
 // This directory is put FIRST on the include path; its softdtw/forward.hpp,
 // backward.hpp and barycenter.hpp all land here.  The reference's real
