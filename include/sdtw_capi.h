@@ -99,6 +99,11 @@ int sdtw_debug_set_trace(sdtw_ctx *ctx, void *trace_dev);
 /* Diagnostics (timing enabled): per phase 0 = not started, 1 = started,
  * 3 = finished (non-blocking event queries; -1 = phase did not run). */
 int sdtw_debug_phase_status(sdtw_ctx *ctx, int *out, int n);
+/* Diagnostics: fp32 fused-mode backward passes of this context (and its
+ * host-call sub-contexts) that read the forward's band cache (out[0]) and,
+ * of those, the ones whose alignment left the band and reran on the tensor
+ * cores (out[1]).  Synchronises the context's stream. */
+int sdtw_debug_band_stats(sdtw_ctx *ctx, unsigned long long *out);
 
 const char *sdtw_last_error(void);
 size_t sdtw_last_oom_bytes(void);

@@ -26,7 +26,8 @@ EXPORTED = [
     "sdtw_ctx_create", "sdtw_ctx_destroy", "sdtw_ctx_set_stream", "sdtw_ctx_stream",
     "sdtw_ctx_synchronize", "sdtw_mem_stats", "sdtw_mem_reset_peak", "sdtw_set_mem_limit",
     "sdtw_mem_trim", "sdtw_launch_count", "sdtw_reset_launch_count", "sdtw_ctx_enable_timing",
-    "sdtw_phase_times", "sdtw_debug_set_trace", "sdtw_debug_phase_status", "sdtw_last_error",
+    "sdtw_phase_times", "sdtw_debug_set_trace", "sdtw_debug_phase_status", "sdtw_debug_band_stats",
+    "sdtw_last_error",
     "sdtw_last_oom_bytes", "sdtw_fwd_bwd_f32", "sdtw_fwd_bwd_f64", "sdtw_forward_f32",
     "sdtw_forward_f64", "sdtw_backward_table_f32", "sdtw_backward_table_f64",
     "sdtw_forward_backward_E_f32", "sdtw_forward_backward_E_f64", "sdtw_input_grads_f32",
@@ -107,6 +108,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sdtw_phase_times": (I, [P, C.POINTER(C.c_float), I]),
         "sdtw_debug_set_trace": (I, [P, P]),
         "sdtw_debug_phase_status": (I, [P, C.POINTER(C.c_int), I]),
+        "sdtw_debug_band_stats": (I, [P, C.POINTER(C.c_ulonglong)]),
         "sdtw_last_oom_bytes": (S, []),
         "sdtw_nccl_get_unique_id": (I, [P]),
         "sdtw_nccl_init": (I, [P, P, I, I]),
@@ -253,6 +255,13 @@ class Engine:
         arr = (C.c_float * len(self.PHASES))()
         _raise(self.lib.sdtw_phase_times(self.ctx, arr, len(self.PHASES)))
         return {k: float(v) for k, v in zip(self.PHASES, arr) if v >= 0}
+
+    def band_stats(self) -> tuple:
+        """(fused backward passes that used the band cache, band misses that
+        reran on the tensor cores) since the context was created."""
+        arr = (C.c_ulonglong * 2)()
+        _raise(self.lib.sdtw_debug_band_stats(self.ctx, arr))
+        return int(arr[0]), int(arr[1])
 
     @property
     def launches(self) -> int:

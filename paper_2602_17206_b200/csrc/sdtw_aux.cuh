@@ -340,4 +340,29 @@ __global__ void normalize_loss_kernel(const T *__restrict__ xx, const T *__restr
     if (b < B) xy[b] = xy[b] - (xx[b] + yy[b]) / T(2);
 }
 
+// Band-cache miss (Dp3Args::band): before the tensor-core backward reruns
+// the call, clear what the void banded pass accumulated (fixed-point
+// gradient sums, the optional dense E, the tile counters).  A no-op unless
+// stats[3] is set.
+template <class T>
+__global__ void band_rerun_clear_kernel(unsigned *stats, unsigned long long *ctr, long long *gx_fx, size_t ngx,
+                                        long long *gy_fx, size_t ngy, long long *rs_fx, size_t nrs, long long *cs_fx,
+                                        size_t ncs, T *E, size_t nE)
+{
+    const bool miss = *reinterpret_cast<volatile unsigned *>(&stats[3]) != 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr[0] += 1;
+        ctr[1] += miss ? 1 : 0;
+    }
+    if (!miss) return;
+    const size_t step = (size_t)gridDim.x * blockDim.x;
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (size_t i = i0; i < ngx; i += step) gx_fx[i] = 0;
+    for (size_t i = i0; i < ngy; i += step) gy_fx[i] = 0;
+    for (size_t i = i0; i < nrs; i += step) rs_fx[i] = 0;
+    for (size_t i = i0; i < ncs; i += step) cs_fx[i] = 0;
+    for (size_t i = i0; i < nE; i += step) E[i] = T(0);
+    if (i0 < 3) stats[i0] = 0u;
+}
+
 }  // namespace sdtw

@@ -123,9 +123,35 @@ struct Dp3Args {
     int4 *tile_meta;               // [B S quota] (b, s, c, width)
     int *strip_tiles;              // [B S] tiles stored per strip
     int tile_quota;
-    unsigned *stats;               // [0] live tiles, [1] tiles stored, [2] overflow (in-warp)
+    unsigned *stats;               // [0] live tiles, [1] tiles stored, [2] overflow (in-warp),
+                                   // [3] band miss (fused band cache, below)
     unsigned long long *trace;     // optional [B*S][2] %globaltimer at strip start / end (forward)
+    // Fused-mode band cache (fp32, tensor-core fused forward): the forward
+    // keeps, per strip, the skewed cost row groups [band_lo, band_lo +
+    // band_ng) around the strip's diagonal (the groups of tiles [-W, W + 2]
+    // from the diagonal, band_ng = 2 W + 4: the backward's speculative
+    // recompute reaches two tiles further right, sdtw_dp4.cuh COMMIT), so the
+    // backward reads them like
+    // the unfused cost tensor instead of recomputing them on the tensor
+    // cores.  A backward tile outside the band sets stats[3]; the tensor-core
+    // backward then reruns the call (band_gate launches exit unless it is
+    // set), so results never depend on the band's width.
+    T *band;                       // [B][S][band_ng][32][32] skewed groups, or null
+    int band_ng;
+    int band_gate;                 // 1: run only if stats[3] != 0
 };
+
+// First cached group of strip s (shared by the forward that fills the band
+// cache and the backward that reads it): the diagonal's chunk at the strip's
+// middle row, W = ng / 2 - 2 groups to the left, clamped into [0, G - ng].
+__host__ __device__ __forceinline__ int band_lo(int s, int N, int M, int G, int ng)
+{
+    const long long mid = 32LL * s + 16;
+    const int cd = (int)((mid * M / (N > 0 ? N : 1)) >> 5);
+    const int lo = cd - (ng / 2 - 2);
+    const int hi = G - ng > 0 ? G - ng : 0;
+    return lo < 0 ? 0 : (lo > hi ? hi : lo);
+}
 
 __device__ __forceinline__ unsigned long long global_ns()
 {

@@ -126,6 +126,9 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ uint32_t tmem_slot;
+    // band-cache rerun: nothing to do unless the banded pass missed the band
+    // (uniform over the grid, before any barrier or TMEM allocation)
+    if (A.band_gate && *reinterpret_cast<volatile unsigned *>(&A.stats[3]) == 0u) return;
     constexpr int kW = bwd_workers<kTc>();
     const DpArgs<T> &a = A.a;
     using SM = Bwd4Smem<T, kFused, kTc, kWin>;
@@ -195,7 +198,13 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
         bool x_loaded = false;
         const float tc_xi = (kTc && row_ok) ? (float)a.xn[(size_t)b * a.N + i - 1] : 0.f;
         const bool bottom = s == a.S - 1;
-        const T *dsrc = kFused ? nullptr : a.dsk + ((size_t)b * a.S + s) * (size_t)a.KK * 32;
+        // unfused: the strip's skewed cost rows; band cache: its cached
+        // groups [glo, glo + band_ng)
+        const bool banded = !kFused && !kTc && A.band != nullptr;
+        const int glo = banded ? band_lo(s, a.N, a.M, ngroups_row, A.band_ng) : 0;
+        const T *dsrc = kFused ? nullptr
+                        : banded ? A.band + ((size_t)b * a.S + s) * (size_t)A.band_ng * 1024
+                                 : a.dsk + ((size_t)b * a.S + s) * (size_t)a.KK * 32;
         unsigned long long *stat_me = stat + ((size_t)b * a.S + s) * a.C;
         const unsigned long long *stat_below = stat + ((size_t)b * a.S + s + 1) * a.C;
         typename TG::Ent *sb_me = A.sbt + ((size_t)b * a.S + s) * a.M;
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
         auto group_of = [&](int cf) {
             for (int g = 0; g < 2; ++g) {
                 const int w0 = ctl[5 + g];
-                if (ctl[7 + g] != 0 && cf <= w0 && cf > w0 - kWin && cf >= 0) return g;
+                if (ctl[7 + g] != 0 && cf <= w0 && cf >= ctl[9 + g] && cf >= 0) return g;
             }
             return -1;
         };
@@ -372,8 +381,25 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
             if constexpr (kTc) {
                 tc_costs(cr, nt, x_loaded, b, s, i, row_ok, tc_xi);
             } else if (!kFused) {
-                for (int g = cr - (kWin - 1); g <= cr + 1; ++g)
-                    if (g >= 0 && g < ngroups_row) load_group(ring + (g & 3) * 1024, dsrc + (size_t)g * 1024, t);
+                for (int g = cr - (kWin - 1); g <= cr + 1; ++g) {
+                    if (g < 0 || g >= ngroups_row) continue;
+                    // left of the band: only the window's speculative tiles
+                    // need it (they are cut off, ctl[9 + g]) unless the
+                    // requested tile cr itself lies there
+                    if (banded && g < glo && cr >= glo) continue;
+                    if (banded && (g < glo || g >= glo + A.band_ng)) {
+                        // outside the cached band: this pass's results are
+                        // void, the tensor-core backward reruns the call
+                        if (t == 0) atomicOr(&A.stats[3], 1u);
+#ifdef SDTW_B5_DEBUG
+                        if (t == 0 && atomicAdd(&A.stats[4], 1u) < 40u)
+                            printf("band miss b=%d s=%d cr=%d nt=%d g=%d glo=%d ng=%d S=%d C=%d\n", b, s, cr, nt, g, glo,
+                                   A.band_ng, a.S, a.C);
+#endif
+                        continue;
+                    }
+                    load_group(ring + (g & 3) * 1024, dsrc + (size_t)(g - glo) * 1024, t);
+                }
                 cp_async_commit();
             }
             T lc[kWin], hp[kWin];
@@ -470,6 +496,10 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                 ctl[7 + g] = 0;
                 __threadfence_block();
                 ctl[5 + g] = cr;
+                // lowest valid tile of the window: a band-cache window stops
+                // at the band's left edge (its tiles further left are never
+                // loaded; E requests them afresh, which then misses the band)
+                ctl[9 + g] = (banded && cr >= glo) ? max(cr - (kWin - 1), glo) : cr - (kWin - 1);
                 __threadfence_block();
                 ctl[7 + g] = 1;
             }
@@ -497,6 +527,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                 }
             }
             cn = __shfl_sync(kFull, cn, 0);
+            if (banded && cn < glo) return false;  // left of the cached band: not speculatively
             return cn >= 0 && serve(cn);
         };
         // ---- E side: ask for a window / wait for a tile's probabilities

@@ -604,6 +604,8 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
             float yn_next = t < a.M ? a.yn[(size_t)b * a.M + t] : 0.f;
             const bool row_ok = row_f <= a.N;
             const int row = row_f;
+            const int glo = A.band ? band_lo(s, a.N, a.M, a.KK / 32, A.band_ng) : 1 << 30;
+            float *band_s = A.band ? A.band + ((size_t)b * a.S + s) * (size_t)A.band_ng * 1024 : nullptr;
             auto fill = [&](int G, auto &lap) {
                 if (G < a.C) {
                     // cost chunk G: TMEM quarter -> epilogue -> skewed ring
@@ -641,6 +643,20 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
                     }
                     __syncwarp();
                     lap(1);
+                }
+                // band cache: group G is complete once chunk G is in (its
+                // other half came with chunk G - 1); entries off the matrix
+                // are stored as zero, like the unfused cost tensor's
+                const int gg = G - glo;
+                if (gg >= 0 && gg < A.band_ng) {
+                    const float *src = ring + (G & 1) * 1024;
+                    float *dst = band_s + (size_t)gg * 1024;
+#pragma unroll 8
+                    for (int r = 0; r < 32; ++r) {
+                        const int col = 32 * G + r - t;
+                        const float v = src[r * 32 + t];
+                        dst[r * 32 + t] = (row_ok && col >= 0 && col < a.M) ? v : 0.f;
+                    }
                 }
             };
             slot_strip_forward(A, b, s, w, base, ring, halo_s, sh.rd[p], sh.hx[p], fill);

@@ -1,0 +1,96 @@
+"""Fused-mode band cache (Dp3Args::band, sdtw_capi.cu Pipeline::plan_band).
+
+The tensor-core fused forward keeps each strip's skewed cost groups for +-W
+tiles around the diagonal (W <= 8, at most a quarter of the cost tensor);
+the backward reads them like the unfused cost tensor.  A backward tile that
+leaves the band voids the pass and the call reruns on the tensor-core
+backward, so results never depend on W:
+
+* band hit (the reference generator's near-diagonal alignments): fused ==
+  unfused bit for bit, and the band was used with no miss;
+* forced miss (W = 0 on N(0,1) data at gamma = 1): the rerun gives the
+  same bits as the band-free fused path and as unfused, incl. the dense E;
+* the band keeps fused mode's peak below unfused by >= 3/4 of the tensor.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+class _env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update({k: str(v) for k, v in self.kv.items()})
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_band_hit_equals_unfused(engine, reference):
+    x, y = reference.bench_inputs(4, 2048, 128)
+    b0 = engine.band_stats()
+    f = engine.sdtw_with_gradients(x, y, 0.01, fused=True)
+    b1 = engine.band_stats()
+    assert b1[0] > b0[0] and b1[1] == b0[1], (b0, b1)  # band used (per pair chunk), no miss
+    u = engine.sdtw_with_gradients(x, y, 0.01)
+    with _env(SDTW_FUSED_BAND=0):
+        t = engine.sdtw_with_gradients(x, y, 0.01, fused=True)
+    assert engine.band_stats() == b1  # the band-free call did not use it
+    for a, b, c in zip(f, u, t):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("dims", [(3, 1024, 900, 64), (2, 777, 1300, 100)])
+def test_band_miss_reruns(engine, dims):
+    B, N, M, D = dims
+    rng = np.random.default_rng(N + M)
+    x = rng.standard_normal((B, N, D)).astype(np.float32)
+    y = rng.standard_normal((B, M, D)).astype(np.float32)
+    with _env(SDTW_FUSED_BAND=0):
+        ref = engine.sdtw_with_gradients(x, y, 1.0, fused=True)
+    b0 = engine.band_stats()
+    with _env(SDTW_FUSED_BAND_W=0):
+        got = engine.sdtw_with_gradients(x, y, 1.0, fused=True)
+    b1 = engine.band_stats()
+    assert b1[0] > b0[0] and b1[1] > b0[1], (b0, b1)  # missed, reran
+    unf = engine.sdtw_with_gradients(x, y, 1.0)
+    for a, b, c in zip(got, ref, unf):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_band_miss_dense_E(engine):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((2, 800, 32)).astype(np.float32)
+    y = rng.standard_normal((2, 800, 32)).astype(np.float32)
+    with _env(SDTW_FUSED_BAND=0):
+        l0, E0 = engine.forward_backward_E(x, y, 0.5, fused=True)
+    with _env(SDTW_FUSED_BAND_W=0):
+        l1, E1 = engine.forward_backward_E(x, y, 0.5, fused=True)
+    assert np.array_equal(l0, l1) and np.array_equal(E0, E1)
+
+
+def test_band_memory_bound(engine, reference):
+    """Peak device bytes: fused (with the band) stays below unfused by at
+    least 3/4 of the B x S x KK x 32 cost tensor (the band is O(B N W),
+    W <= 8, not O(B N M); at the acceptance-criterion-6 size, L = 512, it is
+    off and fused saves the whole tensor, test_parity_gpu.py)."""
+    x, y = reference.bench_inputs(8, 2048, 128)
+    peaks = {}
+    for fused in (False, True):
+        engine.trim()
+        engine.reset_peak()
+        engine.sdtw_with_gradients(x, y, 0.01, fused=fused)
+        peaks[fused] = engine.mem_stats()[1]
+    S, KK = 2048 // 32, ((2048 + 62) // 32) * 32
+    tensor = 8 * S * KK * 32 * 4
+    assert peaks[False] - peaks[True] >= 0.75 * tensor, (peaks, tensor)
