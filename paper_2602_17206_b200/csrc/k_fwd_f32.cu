@@ -12,7 +12,10 @@ KFn<Dp3Args<T>> k_forward3()
 template KFn<Dp3Args<float>> k_forward3<float, 1, false>();
 template KFn<Dp3Args<float>> k_forward3<float, 1, true>();
 
-KFn<Dp3Args<float>, FusedTcArgs> k_forward_tc() { return sdtw_forward_tc_kernel<0>; }
+KFn<Dp3Args<float>, FusedTcArgs> k_forward_tc(bool trace)
+{
+    return trace ? sdtw_forward_tc_kernel<0, true> : sdtw_forward_tc_kernel<0, false>;
+}
 
 SDTW_TU_TIMEOUTS(fwd_f32)
 

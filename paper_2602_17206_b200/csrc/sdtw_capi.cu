@@ -670,11 +670,11 @@ struct Pipeline {
                 plan_band();
                 auto A = args3();
                 const size_t smem = 2 * sdtw::ftc_slot_bytes(dpad);
-                ensure_smem_attr(ctx->device, (const void *)sdtw::k_forward_tc(),
+                ensure_smem_attr(ctx->device, (const void *)sdtw::k_forward_tc(ctx->trace != nullptr),
                                  (int)(2 * sdtw::ftc_slot_bytes(sdtw::kFtcMaxD)));
                 const int work = B * ((S + 3) / 4);
                 const unsigned grid = (unsigned)std::max(1, std::min((work + 1) / 2, ctx->sm_count));
-                launch_ptr(ctx, sdtw::k_forward_tc(), grid, sdtw::kFtcThreads, smem, A, ftc());
+                launch_ptr(ctx, sdtw::k_forward_tc(ctx->trace != nullptr), grid, sdtw::kFtcThreads, smem, A, ftc());
             }
         } else {
             launch_forward3();

@@ -234,7 +234,7 @@ __device__ __forceinline__ void half_chunk_store(const HalfChunk &h, float sc, u
 // the fused kernel's TMEM epilogue or the unfused kernel's cp.async of the
 // cost tensor.
 // ---------------------------------------------------------------------------
-template <class Fill>
+template <bool kTrace, class Fill>
 __device__ __forceinline__ void slot_strip_forward(const Dp3Args<float> &A, int b, int s, int w, unsigned base,
                                                    float *ring, float *halo_s, unsigned *rd,
                                                    unsigned long long (*hx)[kFtcHx], Fill &&fill)
@@ -249,7 +249,9 @@ __device__ __forceinline__ void slot_strip_forward(const Dp3Args<float> &A, int 
     const bool row_ok = row <= a.N;
     // trace: [16 B S + 4 (b S + s) + e]: e = 0 ticket, 1 first 32 columns
     // done, 2 half the columns done, 3 end
-    unsigned long long *trc = A.trace ? A.trace + 16 * (size_t)a.B * a.S + 4 * ((size_t)b * a.S + s) : nullptr;
+    // trace mode is a separate instantiation: the product kernel carries no
+    // clock reads or trace tests on the step path
+    unsigned long long *trc = (kTrace && A.trace) ? A.trace + 16 * (size_t)a.B * a.S + 4 * ((size_t)b * a.S + s) : nullptr;
     if (trc && t == 0) trc[0] = global_ns();
     // cycle accounting (trace mode): [24 B S + 8 (b S + s) + e]:
     // e = 0 cost-tile wait, 1 epilogue, 2 halo wait, 3 back-pressure, 4 steps
@@ -471,7 +473,7 @@ for (int e = 0; e < 5; ++e)
 // tickets and issues the MMAs).  Tickets over super-strips (strip-major,
 // pair-minor) from a.tickets[0].
 // ---------------------------------------------------------------------------
-template <int kTU = 0>
+template <int kTU = 0, bool kTrace = false>
 __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args<float> A, FusedTcArgs F)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -659,7 +661,7 @@ __global__ void __launch_bounds__(kFtcThreads, 1) sdtw_forward_tc_kernel(Dp3Args
                     }
                 }
             };
-            slot_strip_forward(A, b, s, w, base, ring, halo_s, sh.rd[p], sh.hx[p], fill);
+            slot_strip_forward<kTrace>(A, b, s, w, base, ring, halo_s, sh.rd[p], sh.hx[p], fill);
             u += (unsigned)a.C;
         }
     }

@@ -16,7 +16,7 @@ using KFn = void (*)(P...);
 // k_fwd_f32.cu / k_fwd_f64.cu
 template <class T, int K, bool kFused>
 KFn<Dp3Args<T>> k_forward3();
-KFn<Dp3Args<float>, FusedTcArgs> k_forward_tc();
+KFn<Dp3Args<float>, FusedTcArgs> k_forward_tc(bool trace);  // trace: the %globaltimer / clock64 build
 // k_bwd4.cu
 template <class T, bool kFused, bool kTc, int kWin>
 KFn<Dp3Args<T>, unsigned long long *, FusedTcArgs> k_backward4();

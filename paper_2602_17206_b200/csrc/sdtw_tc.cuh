@@ -28,14 +28,21 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+// try_wait suspends the warp until the phase completes or the hint (ns)
+// expires: waiting warps (producers ahead of their consumers, consumers
+// ahead of the MMA) then take no issue slots from the warps they wait for
+#ifndef SDTW_MBAR_SUSPEND_NS
+#define SDTW_MBAR_SUSPEND_NS 0x989680
+#endif
+constexpr uint32_t kMbarSuspendNs = SDTW_MBAR_SUSPEND_NS;
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(kMbarSuspendNs)
         : "memory");
 }
 __device__ __forceinline__ void fence_barrier_init()
