@@ -9,8 +9,9 @@ fused = len(sys.argv) > 2 and sys.argv[2] == "fused"
 B, L, D = cfg["B"], cfg["L"], cfg["D"]
 S = (L + 31) // 32
 eng = Engine(0)
-torch.manual_seed(0)
-x = torch.randn((B, L, D), device="cuda"); y = torch.randn((B, L, D), device="cuda")
+from bench import bench_inputs
+xh, yh = bench_inputs(B, L, D, 42)
+x, y = torch.from_numpy(xh).cuda(), torch.from_numpy(yh).cuda()
 tr = torch.zeros(140 * B * S, dtype=torch.int64, device="cuda")
 for it in range(2):
     eng.lib.sdtw_debug_set_trace(eng.ctx, tr.data_ptr() if it == 1 else None)
@@ -21,9 +22,10 @@ eng.lib.sdtw_debug_set_trace(eng.ctx, None)
 t = tr.cpu().numpy()
 evs = t[40 * B * S:88 * B * S].reshape(B, S, 16, 3)
 t0 = evs[..., 0][evs[..., 0] > 0].min()
-names = {1: "R+", 2: "R-", 3: "E+", 4: "E-", 5: "X"}
+names = {1: "R+", 2: "R-", 3: "E+", 4: "E-", 5: "X", 6: "S", 7: "V"}
 b = 0
-for s in range(S - 1, max(-1, S - 9), -1):
+mid = int(sys.argv[3]) if len(sys.argv) > 3 else S - 1
+for s in range(mid, max(-1, mid - 8), -1):
     line = []
     for k in range(16):
         tm, ch, kd = evs[b, s, k]
