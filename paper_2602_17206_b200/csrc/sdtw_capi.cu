@@ -610,6 +610,12 @@ struct Pipeline {
         A.tile_quota = tile_quota;
         A.stats = stats.p;
         A.trace = ctx->trace;
+        {
+            // verdict-free sweeps near the diagonal (sdtw_dp4.cuh); the
+            // variable is an A/B switch for experiments
+            const char *r = std::getenv("SDTW_BWD_SPEC_RIGHT");
+            A.spec_right = r ? std::atoi(r) : 2;
+        }
         A.band = band.p;
         A.band_ng = band_ng;
         A.band_gate = 0;

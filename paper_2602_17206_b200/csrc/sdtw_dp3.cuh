@@ -136,6 +136,7 @@ struct Dp3Args {
     // cores.  A backward tile outside the band sets stats[3]; the tensor-core
     // backward then reruns the call (band_gate launches exit unless it is
     // set), so results never depend on the band's width.
+    int spec_right;                // sdtw_dp4.cuh: verdict-free sweeps up to this many chunks right of the diagonal
     T *band;                       // [B][S][band_ng][32][32] skewed groups, or null
     int band_ng;
     int band_gate;                 // 1: run only if stats[3] != 0
@@ -144,10 +145,15 @@ struct Dp3Args {
 // First cached group of strip s (shared by the forward that fills the band
 // cache and the backward that reads it): the diagonal's chunk at the strip's
 // middle row, W = ng / 2 - 2 groups to the left, clamped into [0, G - ng].
-__host__ __device__ __forceinline__ int band_lo(int s, int N, int M, int G, int ng)
+// the diagonal's chunk at strip s's middle row
+__host__ __device__ __forceinline__ int diag_chunk(int s, int N, int M)
 {
     const long long mid = 32LL * s + 16;
-    const int cd = (int)((mid * M / (N > 0 ? N : 1)) >> 5);
+    return (int)((mid * M / (N > 0 ? N : 1)) >> 5);
+}
+__host__ __device__ __forceinline__ int band_lo(int s, int N, int M, int G, int ng)
+{
+    const int cd = diag_chunk(s, N, M);
     const int lo = cd - (ng / 2 - 2);
     const int hi = G - ng > 0 ? G - ng : 0;
     return lo < 0 ? 0 : (lo > hi ? hi : lo);

@@ -561,7 +561,9 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                     __threadfence_block();
                     return base + kSlot * (kWin * g + (w0 - cf));
                 }
-                if (g < 0 && !requested) {
+                // (re-)request while the tile is in no group: a window the
+                // helper placed may be evicted before this warp saw it
+                if (g < 0 && (!requested || (polls & 255u) == 255u)) {
                     request(cf);
                     requested = true;
                 }
@@ -650,7 +652,14 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                     continue;
                 }
                 unsigned st0 = __shfl_sync(kFull, st, 0);
-                if (st0 >= kTileCommit) {
+                if (st0 >= kTileCommit && c <= diag_chunk(s, a.N, a.M) + A.spec_right) {
+                    // near the diagonal (where the alignment band lies): sweep
+                    // right behind the strip below, whose S arrives per 8
+                    // columns (zeros if the tile turns out dead), instead of
+                    // waiting for its verdict; the diagonal bound keeps these
+                    // sweeps from cascading over dead tiles
+                    request(c);
+                } else if (st0 >= kTileCommit) {
                     // the strip below has no evidence yet: recompute early (and
                     // say so one level up), then wait for its verdict
                     request(c);
@@ -684,7 +693,17 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
             if (t == 0) put_status(stat_me + c, hinted ? kTileHint : kTileCommit, epoch);
             const int j0 = 32 * c + 1;
             const int width = min(32, a.M - 32 * c);
+            // the whole tile's S from below in one load per lane, issued before
+            // the probability wait: when the strip below has already finished
+            // this tile, the sweep then polls L2 once per tile, not once per
+            // 8 columns (fp32; otherwise per 8 columns as below)
+            unsigned long long s_all = 0;
+            if constexpr (sizeof(T) == 4)
+                if (!bottom && t < width) s_all = TG::load_raw(sb_below + (j0 - 1) + t);
             T *Pc = tile_P(c);
+            bool s_all_ok = false;
+            if constexpr (sizeof(T) == 4)
+                s_all_ok = !bottom && __all_sync(kFull, t >= width || (unsigned)(s_all >> 32) == epoch);
             // ---- phase E with 8-column hand-offs --------------------------
             const bool has_end_tile = bottom && c == a.C - 1;
             T s_prev = T(0);
@@ -717,6 +736,9 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                     T v = T(0);
                     if (!bottom) {
                         if constexpr (sizeof(T) == 4) {
+                          if (s_all_ok) {
+                            v = __uint_as_float((unsigned)(__shfl_sync(kFull, s_all, (lo + t) & 31) & 0xffffffffull));
+                          } else {
                             bool ok = t >= n;
                             if (!ok) {
                                 const unsigned long long w8 = (pf_q == q8) ? pf_w : TG::load_raw(sb_below + (j0 - 1) + lo + t);
@@ -731,6 +753,7 @@ __global__ void __launch_bounds__(64 * bwd_workers<kTc>(), 1) sdtw_backward4_ker
                                 if (t <= jn - lo2) pf_w = TG::load_raw(sb_below + (j0 - 1) + lo2 + t);
                                 pf_q = q8 + 8;
                             }
+                          }
                         } else {
                             v = poll_entries<T>(sb_below + (j0 - 1) + lo, n, epoch, t);
                         }
