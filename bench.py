@@ -52,7 +52,19 @@ CONFIGS = {
 }
 METRIC = "DP cells/sec (fwd+bwd, fused & unfused) at B=32 vs L,D; peak HBM MB; 1/2/4/8 GPU"
 SM_COUNT = 148
-MUFU_PER_CLK_SM = 16
+MUFU_PER_CLK_SM = 16  # ex2 / lg2 / rcp lanes per clock per SM
+
+
+def _mufu_rate():
+    """MUFU lane-ops per clock per SM, measured on this GPU model by
+    scripts/micro/mufu_rate.cu (profiles/mufu_r2.json), else the nominal 16."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "mufu_r2.json")) as fh:
+            m = json.load(fh)
+        r = min(m["ex2_per_clk_sm"], m["lg2_per_clk_sm"], m["rcp_per_clk_sm"])
+        return round(r), f"measured {r:.2f}/clk/SM (profiles/mufu_r2.json)"
+    except Exception:
+        return MUFU_PER_CLK_SM, "nominal"
 # SURVEY.md §8(d): algorithmic MUFU work per DP cell
 MUFU_FWD, MUFU_BWD = 3, 4
 
@@ -549,7 +561,8 @@ def run_engine_arm(args, cfg):
     # ---- roofline of the dominant kernel --------------------------------
     peaks, src = _peaks()
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    mufu_peak = SM_COUNT * MUFU_PER_CLK_SM * sm_mhz * 1e6 / 1e9  # G MUFU op/s
+    mufu_clk, mufu_src = _mufu_rate()
+    mufu_peak = SM_COUNT * mufu_clk * sm_mhz * 1e6 / 1e9  # G MUFU op/s
     per_step = {k: v / args.steps for k, v in phases.items()}
     dom = max(per_step, key=per_step.get) if per_step else "backward"
     roofline = None
@@ -566,7 +579,7 @@ def run_engine_arm(args, cfg):
                                    "whose E is not exactly zero, so its dense-equivalent rate "
                                    "is reported" if dom == "backward" else
                                    f"{mufu} MUFU/cell x {cells_per_rank} cells per launch (SURVEY.md §8(d))",
-                    "peak_basis": f"{SM_COUNT} SM x {MUFU_PER_CLK_SM} MUFU/clk x {sm_mhz} MHz "
+                    "peak_basis": f"{SM_COUNT} SM x {mufu_clk} MUFU/clk ({mufu_src}) x {sm_mhz} MHz "
                                   f"(sm_max_mhz, {src})",
                     "share_of_step": per_step[dom] / (total_ms / args.steps)}
     elif dom == "grads":

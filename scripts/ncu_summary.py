@@ -7,7 +7,8 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 
          "msecond": 1e3, "nsecond": 1e-3, "%": 1}
 KEYS = {"full_c2_backward": "c2_unfused_backward", "full_c3_forward": "c3_unfused_forward",
         "full_c3f_forward": "c3_fused_forward", "full_c4_grads": "c4_unfused_grads",
-        "full_c3_costs": "c3_unfused_costs"}
+        "full_c3_costs": "c3_unfused_costs", "full_c3f_backward": "c3_fused_backward",
+        "full_c3f_grads": "c3_fused_grads"}
 rows_out, traffic = [], {}
 tpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
 if os.path.exists(tpath):
