@@ -803,13 +803,36 @@ struct Pipeline {
             const int ns = B * S, nc = B * C, nkb = (D + kw - 1) / kw;
             const unsigned cg = (unsigned)ctx->sm_count * 8;
             auto contract = kw == 64 ? sdtw::contract_ordered_kernel<T, 64> : sdtw::contract_ordered_kernel<T, 128>;
-            if (gx)
-                LAUNCH(ctx, contract, std::min<unsigned>(ns * nkb, cg), 256, 0, tiles.p,
-                       tile_meta.p, strip_tiles.p, tile_quota, nullptr, nullptr, 0, B, S, C, N, M, D, x, y, gx);
+            // fp32 with 64 < D <= 128: the dot products on tcgen05
+            // (sdtw_grad_tc.cuh; C3 0.266 -> 0.249 ms, C2 0.075 -> 0.067, C1
+            // equal); D = 64 and D > 128 measured faster on the ordered FMA
+            // kernel (C5 4.04 vs 4.17 ms per Adam step, C4 0.103 vs 0.118 ms:
+            // half-empty M = 128 tiles, and per-128-feature items that reload
+            // their E tiles), and fp64 has no tensor-core path.
+            // SDTW_CONTRACT_SIMT=1 / =0 force either kernel (A/B, tests).
+            const char *simt_env = std::getenv("SDTW_CONTRACT_SIMT");
+            bool tc_contract = std::is_same<T, float>::value && D > 64 && D <= 128;
+            if (simt_env) tc_contract = std::is_same<T, float>::value && std::strcmp(simt_env, "0") == 0;
+            auto run_contract = [&](int which, const int *offp, const int *ordp, const T *vout, const T *vpart, T *grad,
+                                    int nbuckets) {
+                if constexpr (std::is_same<T, float>::value) {
+                    if (tc_contract) {
+                        const int items = nbuckets * ((D + 127) / 128);
+                        ensure_smem_attr(ctx->device, (const void *)sdtw::k_contract_tc(), (int)sdtw::kContractTcSmem);
+                        launch_ptr(ctx, sdtw::k_contract_tc(), (unsigned)std::min(items, ctx->sm_count),
+                                   sdtw::kContractTcThreads, sdtw::kContractTcSmem, tiles.p, tile_meta.p, strip_tiles.p,
+                                   tile_quota, offp, ordp, which, B, S, C, N, M, D, vout, vpart,
+                                   (const unsigned *)absmax.p, grad);
+                        return;
+                    }
+                }
+                LAUNCH(ctx, contract, std::min<unsigned>(nbuckets * nkb, cg), 256, 0, tiles.p, tile_meta.p,
+                       strip_tiles.p, tile_quota, offp, ordp, which, B, S, C, N, M, D, vout, vpart, grad);
+            };
+            if (gx) run_contract(0, nullptr, nullptr, x, y, gx, ns);
             if (gy && S <= sdtw::max_list_strips<T>()) {
                 // chunk buckets built inside the contraction (strip order)
-                LAUNCH(ctx, contract, std::min<unsigned>(nc * nkb, cg), 256, 0, tiles.p, tile_meta.p, strip_tiles.p,
-                       tile_quota, nullptr, nullptr, 1, B, S, C, N, M, D, y, x, gy);
+                run_contract(1, nullptr, nullptr, y, x, gy, nc);
             } else if (gy) {
                 Buf<int> cnt(ctx, (size_t)nc), off(ctx, (size_t)nc + 1), ord(ctx, cap);
                 CUDA_OK(cudaMemsetAsync(cnt.p, 0, cnt.n * sizeof(int), ctx->stream));
@@ -819,8 +842,7 @@ struct Pipeline {
                 LAUNCH(ctx, sdtw::tile_scatter_kernel<0>, tg, 256, 0, tile_meta.p, strip_tiles.p, tile_quota, ns, C,
                        off.p, cnt.p, ord.p);
                 LAUNCH(ctx, sdtw::segment_sort_kernel<0>, grid_for(nc, 128), 128, 0, off.p, ord.p, tile_meta.p, nc);
-                LAUNCH(ctx, contract, std::min<unsigned>(nc * nkb, cg), 256, 0, tiles.p,
-                       tile_meta.p, strip_tiles.p, tile_quota, off.p, ord.p, 1, B, S, C, N, M, D, y, x, gy);
+                run_contract(1, off.p, ord.p, y, x, gy, nc);
             }
             if (need_fx) {
                 if (gx)

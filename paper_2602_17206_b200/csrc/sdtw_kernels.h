@@ -24,6 +24,11 @@ KFn<Dp3Args<T>, unsigned long long *, FusedTcArgs> k_backward4();
 KFn<const uint8_t *, const uint8_t *, const float *, const float *, const unsigned *, int, int, int, int, int, int,
     int, int, float *>
 k_cost_gemm();
+KFn<const float *, const int4 *, const int *, int, const int *, const int *, int, int, int, int, int, int, int,
+    const float *, const float *, const unsigned *, float *>
+k_contract_tc();
+constexpr int kContractTcThreads = 512;  // kCtThreads (sdtw_grad_tc.cuh)
+constexpr size_t kContractTcSmem = 4 * 2 * (2 * 128 * 32 * 2 + 2 * 32 * 32 * 2);  // kCtGroups x kCtGroupSmem
 
 // dependency waits that gave up, per translation unit (read and cleared)
 int take_timeouts_fwd_f32();
