@@ -640,6 +640,16 @@ struct Pipeline {
         }
     }
 
+    // recompute window of the backward (sdtw_dp4.cuh bwd_window): 3 tiles per
+    // request where alignment bands are narrow and strips few, 2 (three
+    // workers per SM) where bands are wide or strips many; SDTW_BWD_WIN=2|3
+    // overrides (A/B)
+    static bool bwd_win2(double g, size_t strips)
+    {
+        if (const char *e = std::getenv("SDTW_BWD_WIN")) return std::atoi(e) == 2;
+        return g >= 0.5 || strips > 8192;
+    }
+
     // Band cache width: tiles [-W, W + 2] around the diagonal, W at most 8
     // and the cache at most a quarter of the cost tensor's bytes (so fused
     // mode still saves >= 3/4 of the tensor; at the acceptance-criterion-6
@@ -735,7 +745,7 @@ struct Pipeline {
             Phase ph(ctx, 3);
             if (tc_fused && band.p) {
                 // banded pass: the unfused backward on the cached groups
-                const bool win2 = gamma >= 0.5 || (size_t)B * S > 8192;
+                const bool win2 = bwd_win2(gamma, (size_t)B * S);
                 auto kern = win2 ? sdtw::k_backward4<T, false, false, 2>() : sdtw::k_backward4<T, false, false, 3>();
                 const size_t smem = (win2 ? sdtw::Bwd4Smem<T, false, false, 2>::kPerWarp
                                           : sdtw::Bwd4Smem<T, false, false, 3>::kPerWarp) *
@@ -786,7 +796,7 @@ struct Pipeline {
                 // are narrow and strips few (C2: 0.447 vs 0.455 ms, C3: 1.63
                 // vs 1.72 ms), 2 (three workers per SM) where bands are wide
                 // or strips many (C1 backward -16 %, C5 -25 %)
-                const bool win2 = gamma >= 0.5 || (size_t)B * S > 8192;
+                const bool win2 = bwd_win2(gamma, (size_t)B * S);
                 auto kern = win2 ? sdtw::k_backward4<T, false, false, 2>() : sdtw::k_backward4<T, false, false, 3>();
                 const size_t smem = (win2 ? sdtw::Bwd4Smem<T, false, false, 2>::kPerWarp
                                           : sdtw::Bwd4Smem<T, false, false, 3>::kPerWarp) *
