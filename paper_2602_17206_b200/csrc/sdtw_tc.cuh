@@ -286,7 +286,38 @@ __global__ void __launch_bounds__(256) norms_absmax_f32_kernel(const float *__re
     const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
     float mx = 0.f;
     int pair = -1;
-    for (int r = r0 + w; r < r1; r += 8) {
+    int r = r0 + w;
+    if ((D & 3) == 0 && D <= 128) {
+        // four rows per warp iteration, their loads issued together (one
+        // load latency per four rows instead of per row)
+        for (; r + 24 < r1; r += 32) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                v[u] = 4 * lane < D ? __ldg(reinterpret_cast<const float4 *>(x + (size_t)(r + 8 * u) * D + 4 * lane))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int ru = r + 8 * u;
+                if (ru / rpp != pair) {
+                    if (pair >= 0 && lane == 0 && mx > 0.f) atomicMax(absmax + 2 * pair + which, __float_as_uint(mx));
+                    pair = ru / rpp;
+                    mx = 0.f;
+                }
+                double sd = 0.0;
+                sd = fma((double)v[u].x, (double)v[u].x, sd);
+                sd = fma((double)v[u].y, (double)v[u].y, sd);
+                sd = fma((double)v[u].z, (double)v[u].z, sd);
+                sd = fma((double)v[u].w, (double)v[u].w, sd);
+                float m = fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w)));
+                for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(kFull, sd, o);
+                for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+                mx = fmaxf(mx, m);
+                if (lane == 0) out[ru] = (float)sd;
+            }
+        }
+    }
+    for (; r < r1; r += 8) {
         if (r / rpp != pair) {
             if (pair >= 0 && lane == 0 && mx > 0.f) atomicMax(absmax + 2 * pair + which, __float_as_uint(mx));
             pair = r / rpp;
