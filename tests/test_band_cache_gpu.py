@@ -94,3 +94,21 @@ def test_band_memory_bound(engine, reference):
     S, KK = 2048 // 32, ((2048 + 62) // 32) * 32
     tensor = 8 * S * KK * 32 * 4
     assert peaks[False] - peaks[True] >= 0.75 * tensor, (peaks, tensor)
+
+
+@pytest.mark.parametrize("N,M,bw", [(1500, 1100, 0), (1200, 1200, 100), (900, 1400, 520)])
+def test_band_cache_shapes_and_sakoe_chiba(engine, N, M, bw):
+    """Non-square pairs (the band follows the scaled diagonal) and a
+    Sakoe-Chiba band: the fused result equals unfused bit for bit, hit or
+    miss."""
+    rng = np.random.default_rng(N + 3 * M + bw)
+    t = np.linspace(0, 6, max(N, M))
+    base = np.stack([np.sin(t * (k + 1)) for k in range(64)], axis=1).astype(np.float32)
+    x = (base[np.linspace(0, len(t) - 1, N).astype(int)][None] + 0.05 * rng.standard_normal((2, N, 64))).astype(np.float32)
+    y = (base[np.linspace(0, len(t) - 1, M).astype(int)][None] + 0.05 * rng.standard_normal((2, M, 64))).astype(np.float32)
+    b0 = engine.band_stats()
+    f = engine.sdtw_with_gradients(x, y, 0.05, bandwidth=bw, fused=True)
+    assert engine.band_stats()[0] > b0[0]
+    u = engine.sdtw_with_gradients(x, y, 0.05, bandwidth=bw)
+    for a, c in zip(f, u):
+        assert np.array_equal(a, c)
