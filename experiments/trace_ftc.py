@@ -9,8 +9,10 @@ B, L, D = cfg["B"], cfg["L"], cfg["D"]
 S = (L + 31) // 32
 C = S
 eng = Engine(0)
-x = torch.randn((B, L, D), device="cuda"); y = torch.randn((B, L, D), device="cuda")
-tr = torch.zeros(32 * B * S, dtype=torch.int64, device="cuda")
+from bench import bench_inputs
+xh, yh = bench_inputs(B, L, D, 42)
+x, y = torch.from_numpy(xh).cuda(), torch.from_numpy(yh).cuda()
+tr = torch.zeros(140 * B * S, dtype=torch.int64, device="cuda")  # forward and backward trace slots
 eng.lib.sdtw_debug_set_trace(eng.ctx, tr.data_ptr())
 for _ in range(2):
     tr.zero_()
@@ -34,3 +36,7 @@ print("ticket->first: median %.1f us" % np.median(first - tick))
 print("pair 0 first:", np.round(first[0, :12], 1))
 print("pair 0 end:  ", np.round(end[0, :12], 1))
 print("total span us %.1f" % end.max())
+# how busy the slots are over time: strips in flight (ticket .. end) per 100 us
+span = end.max()
+for q in np.arange(0, span, span / 12):
+    print("t=%7.1f us  strips in flight %5d" % (q, int(((tick <= q) & (end > q)).sum())))
