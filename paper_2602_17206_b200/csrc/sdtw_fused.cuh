@@ -4,9 +4,13 @@
 // the series and the norm cache (cost.hpp:63-78, 112-121) instead of reading
 // a materialised B x N x M tensor (cost.hpp:82-109).  Here the fused forward
 // and the fused backward compute 128 x 32 (forward) or 32 x 32 (backward)
-// cost blocks with tcgen05.mma from fp16 hi/lo operand blocks staged in
-// shared memory by bulk copies (TMA), with fp32 accumulators in TMEM, and
-// feed them straight into the DP: no cost tensor reaches HBM.
+// cost blocks with tcgen05.mma from fp16 hi/lo operand blocks that producer
+// warps stage in shared memory (fp32 rows loaded and split on the fly), with
+// fp32 accumulators in TMEM, and feed them straight into the DP: no cost
+// tensor reaches HBM.  The forward also keeps each strip's cost groups of a
+// narrow band around the diagonal (the band cache, Dp3Args::band: O(B N W)
+// bytes) for the backward, which falls back to recomputing on the tensor
+// cores (sdtw_dp4.cuh, kTc) when an alignment leaves the band.
 //
 // Bit-compatibility.  Each cost is the same instruction sequence as the
 // unfused tcgen05 GEMM (cost_gemm_tc_kernel): K steps of 16 in increasing
@@ -18,13 +22,14 @@
 //
 // Forward CTA: 1 per SM, two independent "slots".  A slot owns a super-strip
 // of 128 rows (4 DP strips, warp w of the slot = strip w = TMEM lane quarter
-// w) of one pair; a producer warp per slot streams 32-column Y chunks in and
-// issues the MMAs into an 8-deep ring of 128 x 32 TMEM tiles; each DP warp
+// w) of one pair; two producer warps per slot stage the super-strip's X rows
+// once and stream 32-column Y chunks in, and the first of them issues the
+// MMAs into an 8-deep ring of 128 x 32 TMEM tiles; each DP warp
 // reads its quarter of chunk G with tcgen05.ld when it starts skewed group G,
 // applies the epilogue and writes the two skewed groups the chunk feeds into
 // its private shared-memory ring, from which the forward step body (the v3
 // one) runs.  Strips of one slot hand the bottom-row h to the strip below
-// through shared memory (64-column ring + progress counters) instead of L2;
+// through shared memory (32-column ring + progress counters) instead of L2;
 // the slot's top strip polls the previous super-strip's tagged halo as v3.
 #pragma once
 #include <type_traits>
