@@ -535,6 +535,9 @@ struct Pipeline {
         ensure_smem_attr(ctx->device, (const void *)kern, (int)smem);
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
         if (occ < 1) fail(SDTW_ECUDA, "DP kernel does not fit on an SM");
+        if (std::getenv("SDTW_DEBUG_OCC"))
+            std::fprintf(stderr, "[sdtw] persistent grid: %d threads, %zu B smem -> %d CTAs per SM\n", threads,
+                         smem, occ);
         const int wpc = threads / 32;
         const int need = (work_warps + wpc - 1) / wpc;
         return (unsigned)std::max(1, std::min(need, occ * ctx->sm_count));
