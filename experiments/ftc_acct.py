@@ -8,7 +8,7 @@ eng = Engine(0)
 torch.manual_seed(0)
 S = (N + 31) // 32
 x = torch.randn((B, N, D), device="cuda"); y = torch.randn((B, M, D), device="cuda")
-tr = torch.zeros(32 * B * S, dtype=torch.int64, device="cuda")
+tr = torch.zeros(140 * B * S, dtype=torch.int64, device="cuda")  # forward and backward trace slots
 eng.enable_timing(True)
 for it in range(3):
     if it == 2:
@@ -25,3 +25,6 @@ names = ["tile-wait", "epilogue", "halo-wait", "backpressure", "steps"]
 med = np.median(cy.reshape(-1, 5), axis=0) / steps
 print(os.environ.get("SDTW_LIB", "main"), f"B={B} N={N} M={M}", "phases(untraced)", {k: round(v, 3) for k, v in ph.items()})
 print("   cycles/step:", dict(zip(names, [round(float(v), 1) for v in med])), "sum", round(float(med.sum()), 1))
+for w in range(4):
+    mw = np.median(cy[:, w::4].reshape(-1, 5), axis=0) / steps
+    print("   strip%%4 == %d:" % w, dict(zip(names, [round(float(v), 1) for v in mw])))
