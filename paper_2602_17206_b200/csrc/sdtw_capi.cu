@@ -658,10 +658,12 @@ struct Pipeline {
     // mode still saves >= 3/4 of the tensor; at the acceptance-criterion-6
     // size, acceptance.cpp:201-229, it is off); none below W = 2.
     // SDTW_FUSED_BAND=0 disables it, SDTW_FUSED_BAND_W=w sets W (tests).
+    bool backward_follows = true;  // forward-only calls keep no band cache
     void plan_band()
     {
         band = Buf<T>();
         band_ng = 0;
+        if (!backward_follows) return;
         const char *off = std::getenv("SDTW_FUSED_BAND");
         if (off && std::strcmp(off, "0") == 0) return;
         const int G = KK / 32;
@@ -1071,6 +1073,7 @@ int forward_api(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_
             ldev = ltmp.p;
         }
         Pipeline<T> pl(ctx, xi.p, yi.p, B, N, M, D, cfg);
+        pl.backward_follows = false;
         pl.norms();
         pl.costs();
         loss_out<T>(pl, ldev);
@@ -1081,12 +1084,14 @@ int forward_api(sdtw_ctx *ctx, const T *x, const T *y, size_t B, size_t N, size_
             Buf<T> lxx(ctx, B), lyy(ctx, B);
             {
                 Pipeline<T> px(ctx, xi.p, xi.p, B, N, N, D, &plain);
+                px.backward_follows = false;
                 px.norms();
                 px.costs();
                 loss_out<T>(px, lxx.p);
             }
             {
                 Pipeline<T> py(ctx, yi.p, yi.p, B, M, M, D, &plain);
+                py.backward_follows = false;
                 py.norms();
                 py.costs();
                 loss_out<T>(py, lyy.p);
