@@ -1,6 +1,6 @@
 // doctest.h — the subset of doctest the reference's unit suite uses
-// (TEST_CASE, CHECK, CHECK_NOTHROW, CHECK_THROWS_AS, doctest::Approx with
-// epsilon), so proj/tests/test_*.cpp compile unchanged without the vendored
+// (TEST_CASE, CHECK, CHECK_FALSE, REQUIRE, CHECK_NOTHROW, CHECK_THROWS_AS,
+// doctest::Approx with epsilon), so proj/tests/test_*.cpp compile unchanged without the vendored
 // header (absent from the reference).  Test infrastructure.
 #pragma once
 #include <cmath>
@@ -79,6 +79,17 @@ inline void fail(const char *file, int line, const char *what)
         ++doctest::detail::checks();                                                     \
         if (!(__VA_ARGS__)) doctest::detail::fail(__FILE__, __LINE__, "CHECK(" #__VA_ARGS__ ")"); \
     } while (0)
+#define CHECK_FALSE(...) CHECK(!(__VA_ARGS__))
+// REQUIRE: a failed requirement ends the test case (doctest throws too)
+namespace doctest { namespace detail { struct RequireFailed {}; } }
+#define REQUIRE(...)                                                                     \
+    do {                                                                                 \
+        ++doctest::detail::checks();                                                     \
+        if (!(__VA_ARGS__)) {                                                            \
+            doctest::detail::fail(__FILE__, __LINE__, "REQUIRE(" #__VA_ARGS__ ")");     \
+            throw doctest::detail::RequireFailed{};                                      \
+        }                                                                                \
+    } while (0)
 #define CHECK_NOTHROW(...)                                                               \
     do {                                                                                 \
         ++doctest::detail::checks();                                                     \
@@ -114,6 +125,8 @@ int main(int argc, char **argv)
         ++cases;
         try {
             c.fn();
+        } catch (const doctest::detail::RequireFailed &) {
+            // recorded by REQUIRE
         } catch (const std::exception &e) {
             doctest::detail::fail(c.file, c.line, ("unexpected exception: " + std::string(e.what())).c_str());
         }
