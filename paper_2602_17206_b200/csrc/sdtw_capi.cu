@@ -633,9 +633,13 @@ struct Pipeline {
         auto A = args3();
         const int threads = 128;
         if (fused) {
+            // SIMT costs (fp64, or fp32 with D > 128): one strip warp per CTA,
+            // so few strips (C4: 256) spread over all SMs' load pipes and L1s
+            // instead of packing four per SM (C4 fused forward 21 ms at 64 SMs)
             auto kern = sdtw::k_forward3<T, 1, true>();
-            const size_t smem = 4 * sdtw::Fwd2Smem<T, 1, true>::kPerWarp * sizeof(T);
-            launch_ptr(ctx, kern, persistent_grid(kern, threads, smem, B * S), threads, smem, A);
+            const int fthreads = 32;
+            const size_t smem = sdtw::Fwd2Smem<T, 1, true>::kPerWarp * sizeof(T);
+            launch_ptr(ctx, kern, persistent_grid(kern, fthreads, smem, B * S), fthreads, smem, A);
         } else {
             auto kern = sdtw::k_forward3<T, 1, false>();
             const size_t smem = 4 * sdtw::Fwd2Smem<T, 1, false>::kPerWarp * sizeof(T);

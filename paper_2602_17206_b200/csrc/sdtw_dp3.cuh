@@ -344,7 +344,16 @@ __global__ void __launch_bounds__(128) sdtw_forward3_kernel(Dp3Args<T> A)
                 // SIMT dot products per strip (they do not depend on the DP
                 // state, so they leave the step chain; same values)
                 T dk[K][8];
-                if (kFused) {
+                if constexpr (kFused && K == 1) {
+                    // staged feature blocks (fused_costs_staged, sdtw_dp2.cuh)
+                    T d8[8];
+                    fused_costs_staged<T>(a, b, s0, t, kb, halo_s + SM::kHalo, d8);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const int col = kb + kk - t;
+                        dk[0][kk] = (row_ok[0] && col >= 0 && col < a.M) ? d8[kk] : T(0);
+                    }
+                } else if (kFused) {
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
