@@ -86,3 +86,19 @@ def test_nccl_init_all_rejects_duplicate_devices(engines3):
     from paper_2602_17206_b200.capi import nccl_init_all
     with pytest.raises(SdtwError):
         nccl_init_all(engines3[:2])  # both on device 0
+
+
+def test_sharded_fused_band_cache(engine, engines3):
+    """Fused shards at a length where the band cache is on (each context keeps
+    its own band and band counters): bitwise equal to one context."""
+    from paper_2602_17206_b200.capi import sdtw_with_gradients_multi
+    rng = np.random.default_rng(21)
+    t = np.linspace(0, 6, 1100)[None, :, None]
+    x = (np.sin(t * np.arange(1, 33)) + 0.2 * rng.standard_normal((5, 1100, 32))).astype(np.float32)
+    y = (np.cos(t * np.arange(1, 33)) + 0.2 * rng.standard_normal((5, 1100, 32))).astype(np.float32)
+    one = engine.sdtw_with_gradients(x, y, 0.05, fused=True)
+    b0 = [e.band_stats()[0] for e in engines3[:2]]
+    many = sdtw_with_gradients_multi(engines3[:2], x, y, 0.05, fused=True)
+    assert all(e.band_stats()[0] > c for e, c in zip(engines3[:2], b0))
+    for u, v in zip(one, many):
+        assert np.array_equal(u, v)
